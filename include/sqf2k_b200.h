@@ -156,6 +156,11 @@ int sqf2k_verify(uint64_t start, uint64_t end, uint32_t k_max,
 int sqf2k_recheck(const uint64_t *n, uint64_t count, uint64_t prime_limit,
                   int32_t *k_out);
 
+/* Squarefree flag of each n[i] >= 1 by exact trial division on the GPU
+ * (replaces sieve.py:154-171 is_squarefree_oracle); same prime rule.   */
+int sqf2k_is_squarefree(const uint64_t *n, uint64_t count, uint64_t prime_limit,
+                        uint8_t *out);
+
 /* ---- profiling -------------------------------------------------------- */
 
 /* When enabled every library kernel launch is bracketed by CUDA events on
@@ -166,6 +171,11 @@ int sqf2k_profile_reset(void);
 int sqf2k_profile_read(sqf2k_kstat_t *out, int cap, int *n);
 /* Synchronise the library stream.                                        */
 int sqf2k_sync(void);
+/* The library's cudaStream_t (as void*), for callers that time on it with
+ * their own CUDA events (bench.py wraps it in torch.cuda.ExternalStream). */
+void *sqf2k_stream(void);
+/* Host<->device bytes the library copied since the last profile reset.   */
+int sqf2k_copy_stats(uint64_t *h2d_bytes, uint64_t *d2h_bytes);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,63 @@
+"""Build libsqf2k_b200.so in-tree: hand-written CUDA for sm_100a (B200).
+
+    python -m paper_2411_01964_b200.build [--force] [--verbose]
+
+nvcc cross-compiles without a GPU; the .so lands next to this file so it
+travels with the repository snapshot to the GPU box.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+INCLUDE = PKG.parent / "include"
+LIB = PKG / "libsqf2k_b200.so"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+SOURCES = ["context.cu", "primes.cu", "verify.cu", "scan.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
+         "--expt-relaxed-constexpr", "-shared", "-cudart", "static", "-diag-suppress", "186"]
+
+
+def _inputs() -> list[Path]:
+    return [CSRC / s for s in SOURCES] + sorted(CSRC.glob("*.cuh")) + [INCLUDE / "sqf2k_b200.h"]
+
+
+def up_to_date() -> bool:
+    if not LIB.exists():
+        return False
+    t = LIB.stat().st_mtime
+    return all(p.stat().st_mtime <= t for p in _inputs())
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and up_to_date():
+        return LIB
+    tmp = LIB.with_name(f".{LIB.name}.{os.getpid()}.tmp")
+    cmd = [NVCC, *ARCH, *FLAGS, "-I", str(INCLUDE), "-o", str(tmp),
+           *[str(CSRC / s) for s in SOURCES]]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.verbose))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,165 @@
+// common.cuh -- runtime plumbing of libsqf2k_b200: error reporting across the
+// C ABI, the per-process device context (one GPU, one stream), grow-only
+// device buffers and event-bracketed kernel launches for profiling.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sqf2k_b200.h"
+
+namespace sqf2k {
+
+// ---- errors -----------------------------------------------------------------
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+void set_error(int code, const char *fmt, ...);
+int fail(int code, const char *fmt, ...);
+
+#define SQF2K_CUDA(expr)                                                          \
+    do {                                                                          \
+        cudaError_t e_ = (expr);                                                  \
+        if (e_ != cudaSuccess) {                                                  \
+            int c_ = (e_ == cudaErrorMemoryAllocation) ? SQF2K_ENOMEM : SQF2K_ECUDA; \
+            throw ::sqf2k::Error{c_, std::string(#expr) + ": " + cudaGetErrorString(e_)}; \
+        }                                                                         \
+    } while (0)
+
+// ---- device buffers -----------------------------------------------------------
+
+struct DevBuf {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t n);  // grow-only, contents not preserved
+    void release();
+    template <class T>
+    T *as() const { return static_cast<T *>(ptr); }
+};
+
+// ---- context --------------------------------------------------------------------
+
+struct KStat {
+    std::string name;
+    uint64_t launches = 0;
+    double total_ms = 0.0;
+};
+
+struct Context {
+    int device = -1;
+    int sm_count = 0;
+    size_t smem_optin = 0;
+    cudaStream_t stream = nullptr;
+    std::recursive_mutex mu;
+
+    // profiling: events recorded around launches, resolved lazily
+    bool profiling = false;
+    struct Pending {
+        int stat;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    std::vector<KStat> stats;
+
+    // named scratch buffers reused across calls
+    DevBuf primes_u32, prime_bits, prime_counts, prime_offsets, scan_tmp;
+    DevBuf residues, items, tile_counts, tile_offsets, tile_cursor, hits;
+    DevBuf acc, esc, fail, fail_sorted, window, kvals, bits_out, host_primes;
+    uint64_t h2d_bytes = 0, d2h_bytes = 0;  // copy accounting (bench e2e)
+    uint64_t primes_limit = 0;  // primes_u32 holds all primes <= primes_limit
+    uint64_t primes_count = 0;
+
+    int stat_index(const char *name);
+    cudaEvent_t get_event();
+    void resolve_profile();  // synchronises
+};
+
+Context &ctx();            // throws Error{SQF2K_ENODEV} if not initialised
+Context *ctx_or_null();
+
+// Launch `kernel` on the library stream, bracketed by events when profiling.
+template <class Kernel, class... Args>
+void launch(const char *name, Kernel kernel, dim3 grid, dim3 block, size_t smem,
+            Args... args) {
+    Context &c = ctx();
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (c.profiling) {
+        a = c.get_event();
+        b = c.get_event();
+        SQF2K_CUDA(cudaEventRecord(a, c.stream));
+    }
+    kernel<<<grid, block, smem, c.stream>>>(args...);
+    SQF2K_CUDA(cudaGetLastError());
+    if (c.profiling) {
+        SQF2K_CUDA(cudaEventRecord(b, c.stream));
+        c.pending.push_back({c.stat_index(name), a, b});
+    }
+}
+
+// Counted host<->device copies on the library stream.
+inline void copy_h2d(void *dst, const void *src, size_t n) {
+    Context &c = ctx();
+    SQF2K_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, c.stream));
+    c.h2d_bytes += n;
+}
+inline void copy_d2h(void *dst, const void *src, size_t n) {
+    Context &c = ctx();
+    SQF2K_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, c.stream));
+    c.d2h_bytes += n;
+}
+
+// Wrap an ABI body: maps exceptions to codes, holds the context lock.
+template <class F>
+int guarded(F &&body) {
+    try {
+        Context &c = ctx();
+        std::lock_guard<std::recursive_mutex> lk(c.mu);
+        return body(c);
+    } catch (const Error &e) {
+        set_error(e.code, "%s", e.msg.c_str());
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        set_error(SQF2K_ENOMEM, "host allocation failed");
+        return SQF2K_ENOMEM;
+    } catch (...) {
+        set_error(SQF2K_ECUDA, "unexpected internal error");
+        return SQF2K_ECUDA;
+    }
+}
+
+// ---- small host helpers --------------------------------------------------------
+
+static inline uint64_t isqrt_u64(uint64_t n) {
+    uint64_t r = 0, bit = 1ULL << 62;
+    while (bit > n) bit >>= 2;
+    while (bit) {
+        if (n >= r + bit) {
+            n -= r + bit;
+            r = (r >> 1) + bit;
+        } else {
+            r >>= 1;
+        }
+        bit >>= 2;
+    }
+    return r;
+}
+
+static inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// Largest end the GPU path accepts: p <= 2^31 keeps p^2 < 2^62 in uint64.
+constexpr uint64_t kMaxEnd = 1ULL << 62;
+
+// Ensure ctx().primes_u32 holds every prime <= limit (GPU prime generator).
+void ensure_primes(uint64_t limit);
+
+}  // namespace sqf2k

@@ -1,0 +1,353 @@
+// scan.cu -- L2 min-k scan over a packed bitmap window in HBM
+// (replaces search.py:400-433 scan_segment and search.py:436-460
+// scan_exponents; window rules of search.py:278-316).
+//
+// The window is one device bitmap: zeros | predecessor bits | current bits |
+// zero pad, with current slot 0 at a 128-bit boundary.  One thread owns 128
+// consecutive slots (one uint4): passes k <= 8 (shift < 128 slots) are funnel
+// shifts of the thread's own uint4 and its left neighbour, passes k >= 9 are
+// aligned 128-bit loads 2^(k-8) vectors back.  Per-k counts stay in registers,
+// per-k least n goes through a block-level atomicMin, failures (or, in the
+// two-pass verify pipeline, escalations) are appended to a device list.
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace sqf2k {
+
+uint64_t generate_primes_device(uint64_t limit);
+void finish_summary(sqf2k_summary_t *out, const uint64_t *fail_sorted_head, uint64_t n_fail);
+int deliver_failures(unsigned long long *fail_dev, uint64_t n_fail, uint64_t *failures,
+                     uint64_t fail_cap, uint64_t *smallest);
+
+namespace {
+
+constexpr int kScanThreads = 256;
+
+struct ScanParams {
+    const uint4 *w4;     // window as 128-bit vectors
+    uint64_t c0;         // vector index of current slot 0
+    uint64_t n_slots;
+    uint64_t first_n;    // n of current slot 0
+    uint64_t one_slot;   // slot of n = 1 (excluded), ~0 if none
+    uint32_t k_scan;     // passes
+    uint32_t k_max;      // escalate leftovers when k_max > k_scan
+    unsigned long long *hist, *min_n;
+    unsigned long long *esc, *esc_count;
+    uint64_t esc_cap;
+    unsigned long long *fail, *fail_count;
+    uint64_t fail_cap;
+    uint8_t *kvals;      // exponent-dump mode
+};
+
+__device__ __forceinline__ uint32_t lane_of(const uint4 &v, int i) {
+    return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+template <bool EXPO>
+__global__ void __launch_bounds__(kScanThreads) window_scan_kernel(const ScanParams P) {
+    __shared__ unsigned long long s_first[65];
+    __shared__ unsigned int s_hist[65];
+    for (int k = threadIdx.x; k < 65; k += blockDim.x) {
+        s_first[k] = ~0ull;
+        s_hist[k] = 0;
+    }
+    __syncthreads();
+    uint32_t cnt[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) cnt[k] = 0;
+    const uint64_t n_vec = (P.n_slots + 127) / 128;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n_vec;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 cur = P.w4[P.c0 + v];
+        const uint4 prv = P.w4[P.c0 + v - 1];
+        const uint64_t s0 = 128 * v;
+        uint32_t pend[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            uint64_t a = s0 + 32 * i;
+            uint32_t m = 0;
+            if (a < P.n_slots) m = (a + 32 <= P.n_slots) ? ~0u : ((1u << (uint32_t)(P.n_slots - a)) - 1u);
+            if (P.one_slot >= a && P.one_slot < a + 32) m &= ~(1u << (uint32_t)(P.one_slot - a));
+            pend[i] = m;
+        }
+        const uint32_t wv[6] = {prv.z, prv.w, cur.x, cur.y, cur.z, cur.w};  // words -2..3
+        for (uint32_t k = 1; k <= P.k_scan; ++k) {
+            if (!(pend[0] | pend[1] | pend[2] | pend[3])) break;
+            uint32_t sl[4];
+            if (k <= 5) {
+                const uint32_t s = 1u << (k - 1);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) sl[i] = __funnelshift_l(wv[i + 1], wv[i + 2], s);
+            } else if (k == 6) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) sl[i] = wv[i + 1];
+            } else if (k == 7) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) sl[i] = wv[i];
+            } else if (k == 8) {
+                sl[0] = prv.x; sl[1] = prv.y; sl[2] = prv.z; sl[3] = prv.w;
+            } else {
+                const uint4 b = P.w4[P.c0 + v - (1ull << (k - 8))];
+                sl[0] = b.x; sl[1] = b.y; sl[2] = b.z; sl[3] = b.w;
+            }
+            uint32_t c = 0;
+            uint64_t first = ~0ull;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t nw = pend[i] & sl[i];
+                if (nw) {
+                    c += __popc(nw);
+                    if (first == ~0ull) first = s0 + 32 * i + __ffs(nw) - 1;
+                    if (EXPO)
+                        for (uint32_t x = nw; x; x &= x - 1)
+                            P.kvals[s0 + 32 * i + __ffs(x) - 1] = (uint8_t)k;
+                }
+                pend[i] &= ~sl[i];
+            }
+            if (c) {
+#pragma unroll
+                for (int kk = 1; kk <= 8; ++kk)
+                    if (kk == (int)k) cnt[kk] += c;
+                if (k > 8) atomicAdd(&s_hist[k], c);
+                atomicMin(&s_first[k], first);
+            }
+        }
+        if (!EXPO && (pend[0] | pend[1] | pend[2] | pend[3])) {
+            const bool esc = P.k_max > P.k_scan;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                for (uint32_t x = pend[i]; x; x &= x - 1) {
+                    const uint64_t n = P.first_n + 2 * (s0 + 32 * i + __ffs(x) - 1);
+                    unsigned long long *list = esc ? P.esc : P.fail;
+                    unsigned long long *count = esc ? P.esc_count : P.fail_count;
+                    const uint64_t cap = esc ? P.esc_cap : P.fail_cap;
+                    unsigned long long j = atomicAdd(count, 1ull);
+                    if (j < cap) list[j] = n;
+                }
+        }
+    }
+    if (EXPO) return;
+#pragma unroll
+    for (int k = 1; k <= 8; ++k) {
+        uint32_t s = __reduce_add_sync(0xffffffffu, cnt[k]);
+        if ((threadIdx.x & 31) == 0 && s) atomicAdd(&s_hist[k], s);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < 65; k += blockDim.x) {
+        if (s_hist[k]) atomicAdd(&P.hist[k], (unsigned long long)s_hist[k]);
+        if (s_first[k] != ~0ull)
+            atomicMin(&P.min_n[k], (unsigned long long)(P.first_n + 2 * s_first[k]));
+    }
+}
+
+// Copy predecessor bits (LSB-first bytes, prev_n bits) so that bit i lands at
+// window bit D + i; words [D/32, end_word) are written, bits below D are 0.
+__global__ void place_bits_kernel(const uint32_t *__restrict__ src, uint64_t src_bits,
+                                  uint64_t D, uint64_t end_word, uint32_t *__restrict__ dst) {
+    const uint64_t w_lo = D / 32;
+    for (uint64_t j = w_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < end_word;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t out = 0;
+        for (int b = 0; b < 32; ++b) {
+            uint64_t pos = 32 * j + b;
+            if (pos < D) continue;
+            uint64_t i = pos - D;
+            if (i >= src_bits) break;
+            out |= ((src[i >> 5] >> (i & 31)) & 1u) << b;
+        }
+        dst[j] = out;
+    }
+}
+
+struct ScanAcc {
+    unsigned long long hist[SQF2K_HIST_LEN];
+    unsigned long long min_n[SQF2K_HIST_LEN];
+    unsigned long long esc_count, fail_count;
+};
+
+unsigned grid_for(uint64_t n_vec) {
+    Context &c = ctx();
+    return (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>(ceil_div(n_vec, kScanThreads), (uint64_t)c.sm_count * 8));
+}
+
+// Build the device window of search.py:278-316 (validation already done).
+// Returns the vector index of current slot 0.
+uint64_t build_window(const uint8_t *prev, uint64_t prev_n, const uint8_t *cur, uint64_t cur_n,
+                      uint64_t prev_eff) {
+    Context &c = ctx();
+    const uint64_t P0 = ceil_div(std::max<uint64_t>(prev_eff, 128), 128) * 128;  // bits
+    const uint64_t cur_bytes = ceil_div(cur_n, 64) * 8;
+    const uint64_t total_bits = P0 + ceil_div(cur_n, 128) * 128 + 256;
+    const uint64_t total_bytes = total_bits / 8;
+    const uint64_t prev_bytes = prev ? ceil_div(prev_n, 64) * 8 : 0;
+    c.window.reserve(total_bytes + prev_bytes + 64);
+    uint8_t *w = c.window.as<uint8_t>();
+    SQF2K_CUDA(cudaMemsetAsync(w, 0, total_bytes, c.stream));
+    if (prev && prev_n) {
+        uint8_t *staging = w + total_bytes + (8 - total_bytes % 8) % 8;
+        copy_h2d(staging, prev, prev_bytes);
+        const uint64_t D = P0 - prev_n;
+        const uint64_t nw = P0 / 32 - D / 32;
+        launch("window_place", place_bits_kernel,
+               dim3((unsigned)std::min<uint64_t>(ceil_div(nw, 256), 4096)), dim3(256), 0,
+               (const uint32_t *)staging, prev_n, D, P0 / 32, (uint32_t *)w);
+    }
+    copy_h2d(w + P0 / 8, cur, cur_bytes);
+    return P0 / 128;
+}
+
+// Validation of search.py:219-224 and search.py:288-311; returns the
+// effective predecessor depth (slots) or -1 with the error set.
+int64_t window_depth(const uint8_t *prev, uint64_t prev_start, uint64_t prev_end,
+                     uint64_t cur_start, uint64_t cur_end, uint32_t k_max) {
+    if (cur_start < 1 || cur_start % 2 == 0 || cur_end <= cur_start || (cur_end - cur_start) % 2) {
+        fail(SQF2K_EINVAL, "bad segment bounds [%llu, %llu)", (unsigned long long)cur_start,
+             (unsigned long long)cur_end);
+        return -1;
+    }
+    if (k_max < 1 || k_max > 63) {
+        fail(SQF2K_EINVAL, "k_max must be positive, got %u", k_max);
+        return -1;
+    }
+    const uint64_t need = ceil_div(1ull << (k_max - 1), 64) * 64;
+    if (!prev) {
+        if (cur_start != 1) {
+            fail(SQF2K_EINVAL, "window starting at %llu needs a predecessor segment",
+                 (unsigned long long)cur_start);
+            return -1;
+        }
+        return (int64_t)need;
+    }
+    if (prev_end != cur_start) {
+        fail(SQF2K_EINVAL, "segments not adjacent: previous ends at %llu, current starts at %llu",
+             (unsigned long long)prev_end, (unsigned long long)cur_start);
+        return -1;
+    }
+    const uint64_t pn = (prev_end - prev_start) / 2;
+    if (pn >= need && pn % 64 == 0) return (int64_t)pn;
+    if (prev_start == 1) return (int64_t)std::max(need, ceil_div(pn, 64) * 64);
+    fail(SQF2K_EINVAL, "predecessor [%llu, %llu) is too shallow or unaligned for k_max %u",
+         (unsigned long long)prev_start, (unsigned long long)prev_end, k_max);
+    return -1;
+}
+
+}  // namespace
+
+void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_slots,
+                        uint64_t first_n, uint32_t k_scan, uint32_t k_max, uint64_t one_slot,
+                        unsigned long long *hist, unsigned long long *min_n,
+                        unsigned long long *esc, unsigned long long *esc_count, uint64_t esc_cap,
+                        unsigned long long *fail, unsigned long long *fail_count,
+                        uint64_t fail_cap) {
+    ScanParams P;
+    std::memset(&P, 0, sizeof P);
+    P.w4 = reinterpret_cast<const uint4 *>(words);
+    P.c0 = cur_word0 / 4;
+    P.n_slots = n_slots;
+    P.first_n = first_n;
+    P.one_slot = one_slot;
+    P.k_scan = k_scan;
+    P.k_max = k_max;
+    P.hist = hist;
+    P.min_n = min_n;
+    P.esc = esc;
+    P.esc_count = esc_count;
+    P.esc_cap = esc_cap;
+    P.fail = fail;
+    P.fail_count = fail_count;
+    P.fail_cap = fail_cap;
+    launch("window_scan", window_scan_kernel<false>, dim3(grid_for(ceil_div(n_slots, 128))),
+           dim3(kScanThreads), 0, P);
+}
+
+}  // namespace sqf2k
+
+using namespace sqf2k;
+
+extern "C" int sqf2k_scan_window(const uint8_t *prev_bits, uint64_t prev_start, uint64_t prev_end,
+                                 const uint8_t *cur_bits, uint64_t cur_start, uint64_t cur_end,
+                                 uint32_t k_max, sqf2k_summary_t *out, uint64_t *failures,
+                                 uint64_t fail_cap) {
+    int64_t depth = window_depth(prev_bits, prev_start, prev_end, cur_start, cur_end, k_max);
+    if (depth < 0) return SQF2K_EINVAL;
+    return guarded([&](Context &c) -> int {
+        const uint64_t cur_n = (cur_end - cur_start) / 2;
+        const uint64_t prev_n = prev_bits ? (prev_end - prev_start) / 2 : 0;
+        uint64_t dev_cap = std::max<uint64_t>(fail_cap, 1 << 12);
+        for (int attempt = 0; attempt < 3; ++attempt) {
+            const uint64_t c0 = build_window(prev_bits, prev_n, cur_bits, cur_n, (uint64_t)depth);
+            c.acc.reserve(sizeof(ScanAcc));
+            c.fail.reserve(dev_cap * 8);
+            ScanAcc init;
+            std::memset(&init, 0, sizeof init);
+            for (int k = 0; k < SQF2K_HIST_LEN; ++k) init.min_n[k] = ~0ull;
+            ScanAcc *acc = c.acc.as<ScanAcc>();
+            copy_h2d(acc, &init, sizeof init);
+            scan_bitmap_device(c.window.as<uint32_t>(), c0 * 4, cur_n, cur_start, k_max, k_max,
+                               cur_start == 1 ? 0 : ~0ull, acc->hist, acc->min_n, nullptr,
+                               &acc->esc_count, 0, c.fail.as<unsigned long long>(),
+                               &acc->fail_count, dev_cap);
+            ScanAcc h;
+            copy_d2h(&h, acc, sizeof h);
+            SQF2K_CUDA(cudaStreamSynchronize(c.stream));
+            if (h.fail_count > dev_cap && h.fail_count <= fail_cap) {
+                dev_cap = h.fail_count;
+                continue;
+            }
+            std::memset(out, 0, sizeof *out);
+            out->start = cur_start;
+            out->end = cur_end;
+            out->k_max = k_max;
+            for (int k = 0; k < SQF2K_HIST_LEN; ++k) {
+                out->hist[k] = h.hist[k];
+                out->min_n[k] = h.min_n[k];
+            }
+            if (h.fail_count > fail_cap) {
+                out->n_failures = h.fail_count;
+                return fail(SQF2K_ECAPACITY, "%llu failures exceed the buffer of %llu",
+                            (unsigned long long)h.fail_count, (unsigned long long)fail_cap);
+            }
+            uint64_t smallest = SQF2K_NONE;
+            deliver_failures(c.fail.as<unsigned long long>(), h.fail_count, failures, fail_cap,
+                             &smallest);
+            finish_summary(out, &smallest, h.fail_count);
+            return SQF2K_OK;
+        }
+        return fail(SQF2K_ECUDA, "scan did not converge on buffer sizes");
+    });
+}
+
+extern "C" int sqf2k_scan_exponents(const uint8_t *prev_bits, uint64_t prev_start,
+                                    uint64_t prev_end, const uint8_t *cur_bits,
+                                    uint64_t cur_start, uint64_t cur_end, uint32_t k_max,
+                                    uint8_t *kvals, uint64_t n_slots) {
+    int64_t depth = window_depth(prev_bits, prev_start, prev_end, cur_start, cur_end, k_max);
+    if (depth < 0) return SQF2K_EINVAL;
+    if (n_slots != (cur_end - cur_start) / 2)
+        return fail(SQF2K_EINVAL, "kvals holds %llu slots, segment has %llu",
+                    (unsigned long long)n_slots, (unsigned long long)((cur_end - cur_start) / 2));
+    return guarded([&](Context &c) -> int {
+        const uint64_t prev_n = prev_bits ? (prev_end - prev_start) / 2 : 0;
+        const uint64_t c0 = build_window(prev_bits, prev_n, cur_bits, n_slots, (uint64_t)depth);
+        c.kvals.reserve(n_slots + 16);
+        SQF2K_CUDA(cudaMemsetAsync(c.kvals.ptr, 0, n_slots, c.stream));
+        ScanParams P;
+        std::memset(&P, 0, sizeof P);
+        P.w4 = reinterpret_cast<const uint4 *>(c.window.ptr);
+        P.c0 = c0;
+        P.n_slots = n_slots;
+        P.first_n = cur_start;
+        P.one_slot = cur_start == 1 ? 0 : ~0ull;
+        P.k_scan = k_max;
+        P.k_max = k_max;
+        P.kvals = c.kvals.as<uint8_t>();
+        launch("window_exponents", window_scan_kernel<true>,
+               dim3(grid_for(ceil_div(n_slots, 128))), dim3(kScanThreads), 0, P);
+        copy_d2h(kvals, c.kvals.ptr, n_slots);
+        SQF2K_CUDA(cudaStreamSynchronize(c.stream));
+        return SQF2K_OK;
+    });
+}
