@@ -149,9 +149,7 @@ def run_ours(args) -> dict | None:
 
     for _ in range(args.warmup):
         step_device()
-    # --- device-timed steps (value) ----------------------------------------
-    _lib.profile(True)
-    _lib.profile_reset()
+    # --- device-timed steps (value): no per-kernel events in the way --------
     times = []
     barrier()
     with ClockSampler(local) as clocks:
@@ -166,6 +164,14 @@ def run_ours(args) -> dict | None:
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
     barrier()
+    # --- per-kernel breakdown: the same steps with every launch bracketed ---
+    _lib.profile(True)
+    _lib.profile_reset()
+    prof_steps = max(3, min(args.steps, 10))
+    for _ in range(prof_steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        step_device()
     kstats = _lib.profile_read()
     _lib.profile(False)
     my_ms = sum(times) / len(times)
@@ -205,13 +211,13 @@ def run_ours(args) -> dict | None:
     name, (launches, total_ms) = top
     per_launch_ms = total_ms / max(launches, 1)
     # one tile launch per batch; C2 is one batch per step
-    units_per_launch = (hi - lo) // 2 * args.steps / max(launches, 1)
+    units_per_launch = (hi - lo) // 2 * prof_steps / max(launches, 1)
     achieved = units_per_launch * BYTES_PER_ODD_N / (per_launch_ms / 1e3) / 1e9
     traffic = None
     tj = ROOT / "profiles" / "ncu_traffic.json"
     if tj.exists():
         traffic = json.loads(tj.read_text()).get(name, {}).get("bytes_per_launch")
-    launches_per_step = sum(v[0] for v in kstats.values()) / args.steps
+    launches_per_step = sum(v[0] for v in kstats.values()) / prof_steps
 
     line = {
         "metric": METRIC,
@@ -239,9 +245,9 @@ def run_ours(args) -> dict | None:
             "frac": achieved / peak, "traffic": traffic,
             "algorithmic_bytes_per_odd_n": BYTES_PER_ODD_N,
             "kernel_ms_per_launch": per_launch_ms,
-            "kernel_share_of_step": total_ms / sum(times),
+            "kernel_share_of_step": (total_ms / prof_steps) / my_ms,
         },
-        "kernels": {k: {"launches_per_step": v[0] / args.steps, "ms_per_step": v[1] / args.steps}
+        "kernels": {k: {"launches_per_step": v[0] / prof_steps, "ms_per_step": v[1] / prof_steps}
                     for k, v in sorted(kstats.items())},
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "e2e": {"value": n_odd / e2e_s, "unit": "odd n/s", "s_per_step": e2e_s,

@@ -20,7 +20,7 @@ INCLUDE = PKG.parent / "include"
 LIB = PKG / "libsqf2k_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["context.cu", "primes.cu", "verify.cu", "scan.cu"]
+SOURCES = ["context.cu", "primes.cu", "tile.cu", "verify.cu", "scan.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-shared", "-cudart", "static", "-diag-suppress", "186"]

@@ -73,8 +73,10 @@ struct Context {
 
     // named scratch buffers reused across calls
     DevBuf primes_u32, prime_bits, prime_counts, prime_offsets, scan_tmp;
-    DevBuf residues, items, tile_counts, tile_offsets, tile_cursor, hits;
+    DevBuf residues, items, tile_counts, tile_offsets, hits;
     DevBuf acc, esc, fail, fail_sorted, window, kvals, bits_out, host_primes;
+    DevBuf pattern, prime_info;
+    void *pinned = nullptr;  // small pinned host staging (summary readback)
     uint64_t h2d_bytes = 0, d2h_bytes = 0;  // copy accounting (bench e2e)
     uint64_t primes_limit = 0;  // primes_u32 holds all primes <= primes_limit
     uint64_t primes_count = 0;
@@ -139,7 +141,7 @@ int guarded(F &&body) {
 
 // ---- small host helpers --------------------------------------------------------
 
-static inline uint64_t isqrt_u64(uint64_t n) {
+__host__ __device__ static inline uint64_t isqrt_u64(uint64_t n) {
     uint64_t r = 0, bit = 1ULL << 62;
     while (bit > n) bit >>= 2;
     while (bit) {
@@ -159,7 +161,12 @@ static inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b
 // Largest end the GPU path accepts: p <= 2^31 keeps p^2 < 2^62 in uint64.
 constexpr uint64_t kMaxEnd = 1ULL << 62;
 
-// Ensure ctx().primes_u32 holds every prime <= limit (GPU prime generator).
-void ensure_primes(uint64_t limit);
+// GPU prime generator: every prime <= limit into ctx().primes_u32 and the
+// PrimeInfo split into ctx().prime_info, without a host sync (async) or
+// returning the count (sync).
+void generate_primes_async(uint64_t limit);
+uint64_t generate_primes_device(uint64_t limit);
+// Upper bound of pi(x) (Rosser-Schoenfeld), for buffer sizing without a sync.
+uint64_t pi_upper(uint64_t x);
 
 }  // namespace sqf2k

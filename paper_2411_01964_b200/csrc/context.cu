@@ -145,6 +145,11 @@ int sqf2k_init(int device) {
         delete c;
         return fail(SQF2K_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
     }
+    if ((e = cudaMallocHost(&c->pinned, 1 << 16)) != cudaSuccess) {
+        cudaStreamDestroy(c->stream);
+        delete c;
+        return fail(SQF2K_ECUDA, "cudaMallocHost: %s", cudaGetErrorString(e));
+    }
     g_ctx = c;
     return SQF2K_OK;
 }
@@ -157,10 +162,11 @@ void sqf2k_shutdown(void) {
     cudaStreamSynchronize(c->stream);
     for (DevBuf *b : {&c->primes_u32, &c->prime_bits, &c->prime_counts, &c->prime_offsets,
                       &c->scan_tmp, &c->residues, &c->items, &c->tile_counts,
-                      &c->tile_offsets, &c->tile_cursor, &c->hits, &c->acc, &c->esc,
+                      &c->tile_offsets, &c->hits, &c->acc, &c->esc,
                       &c->fail, &c->fail_sorted, &c->window, &c->kvals, &c->bits_out,
-                      &c->host_primes})
+                      &c->host_primes, &c->pattern, &c->prime_info})
         b->release();
+    if (c->pinned) cudaFreeHost(c->pinned);
     for (auto &p : c->pending) {
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);

@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "tile.cuh"
 
 namespace sqf2k {
 
@@ -21,6 +22,76 @@ constexpr int kSegOdds = 1 << 16;          // odd numbers per segment
 constexpr int kSegWords = kSegOdds / 32;   // 2048 u32 words
 constexpr int kSieveThreads = 512;
 constexpr int kMaxBase = 6600;             // pi(65536) = 6542 >= pi(isqrt(2^32))
+
+// Split of a table holding every prime <= limit: positional (kPiPow2).
+__device__ void fill_info(PrimeInfo *info, unsigned long long n) {
+    info->count = n;
+    info->i_lo = (uint32_t)min(n, (unsigned long long)kPiBelowPMed);
+    info->i_hi = (uint32_t)n;
+    for (int j = 0; j <= kClasses; ++j) info->cls[j] = (uint32_t)min(n, (unsigned long long)pi_pow2(j));
+}
+
+// Whole table for limit < 2^17 (one segment) in one CTA: base primes, sieve,
+// ordered compaction and the split.
+__global__ void __launch_bounds__(kSieveThreads) prime_small_kernel(uint64_t limit,
+                                                                     uint32_t *__restrict__ out,
+                                                                     PrimeInfo *__restrict__ info) {
+    __shared__ uint32_t w[kSegWords];
+    __shared__ uint32_t base[128];
+    __shared__ uint32_t nbase;
+    const uint32_t r = (uint32_t)isqrt_u64(limit);  // <= 362
+    if (threadIdx.x == 0) {
+        __shared__ uint8_t comp[400];
+        uint32_t nb = 0;
+        for (uint32_t i = 0; i <= r && i < 400; ++i) comp[i] = 0;
+        for (uint32_t p = 3; p <= r; p += 2) {
+            if (comp[p]) continue;
+            base[nb++] = p;
+            for (uint32_t m = p * p; m <= r; m += 2 * p) comp[m] = 1;
+        }
+        nbase = nb;
+    }
+    for (int j = threadIdx.x; j < kSegWords; j += blockDim.x) {
+        const uint64_t m0 = 1 + 64ull * j;  // odd numbers 2i+1, i = 32j..32j+31
+        uint32_t word = 0xffffffffu;
+        if (m0 + 62 > limit) {
+            word = 0;
+            for (int b = 0; b < 32; ++b)
+                if (m0 + 2ull * b <= limit) word |= 1u << b;
+        }
+        if (j == 0) word &= ~1u;  // 1 is not prime
+        w[j] = word;
+    }
+    __syncthreads();
+    for (uint32_t k = 0; k < nbase; ++k) {
+        const uint32_t p = base[k];
+        for (uint32_t i = (p * p - 1) / 2 + threadIdx.x * p; i < (uint32_t)kSegOdds; i += blockDim.x * p)
+            atomicAnd(&w[i >> 5], ~(1u << (i & 31)));
+    }
+    __syncthreads();
+    constexpr int kPer = kSegWords / kSieveThreads;
+    uint32_t v[kPer], cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        v[j] = w[threadIdx.x * kPer + j];
+        cnt += __popc(v[j]);
+    }
+    using Scan = cub::BlockScan<uint32_t, kSieveThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    uint32_t off, total;
+    Scan(tmp).ExclusiveSum(cnt, off, total);
+    uint32_t pos = off + (limit >= 2 ? 1 : 0);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+        for (uint32_t x = v[j]; x; x &= x - 1) {
+            const uint32_t i = (threadIdx.x * kPer + j) * 32 + __ffs(x) - 1;
+            out[pos++] = 2 * i + 1;
+        }
+    if (threadIdx.x == 0) {
+        if (limit >= 2) out[0] = 2;
+        fill_info(info, total + (limit >= 2 ? 1 : 0));
+    }
+}
 
 // Odd base primes 3..r (r <= 65536) into base[], count into *nbase.
 __global__ void __launch_bounds__(1024) base_primes_kernel(uint32_t r, uint32_t *base,
@@ -113,7 +184,8 @@ __global__ void __launch_bounds__(kSieveThreads) prime_segment_kernel(
 // Write the primes of one segment in ascending order at offsets[seg] (+1 for 2).
 __global__ void __launch_bounds__(kSieveThreads) prime_compact_kernel(
     const uint32_t *__restrict__ bits, const uint64_t *__restrict__ offsets,
-    uint32_t *__restrict__ out, int with_two) {
+    uint32_t *__restrict__ out, int with_two, const uint64_t *__restrict__ total,
+    PrimeInfo *__restrict__ info) {
     constexpr int kPer = kSegWords / kSieveThreads;  // 4 words per thread
     const uint32_t *w = bits + (uint64_t)blockIdx.x * kSegWords + threadIdx.x * kPer;
     uint32_t v[kPer], cnt = 0;
@@ -134,7 +206,12 @@ __global__ void __launch_bounds__(kSieveThreads) prime_compact_kernel(
             uint64_t i = i_base + 32 * j + __ffs(x) - 1;
             out[pos++] = (uint32_t)(2 * i + 1);
         }
-    if (with_two && blockIdx.x == 0 && threadIdx.x == 0) out[0] = 2;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (with_two) out[0] = 2;
+        // the table is every prime <= limit: the split is positional
+        const unsigned long long n = *total + (with_two ? 1 : 0);
+        fill_info(info, n);
+    }
 }
 
 __global__ void widen_kernel(const uint32_t *__restrict__ in, int64_t *__restrict__ out, uint64_t n) {
@@ -145,26 +222,40 @@ __global__ void widen_kernel(const uint32_t *__restrict__ in, int64_t *__restric
 
 }  // namespace
 
-// Generate every prime <= limit into ctx.primes_u32; returns the count.
-uint64_t generate_primes_device(uint64_t limit) {
+uint64_t pi_upper(uint64_t x) {
+    // pi(x) < 1.25506 x / ln x for x > 1 (Rosser & Schoenfeld)
+    if (x < 17) return 8;
+    return (uint64_t)(1.25506 * (double)x / std::log((double)x)) + 16;
+}
+
+// Launch the generator for every prime <= limit; count and split land in
+// ctx.prime_info (device), the table in ctx.primes_u32.  No host sync.
+void generate_primes_async(uint64_t limit) {
     Context &c = ctx();
     if (limit > 0xffffffffull) throw Error{SQF2K_EINVAL, "prime limit above 2^32"};
     c.primes_limit = limit;
-    c.primes_count = 0;
     c.primes_u32.reserve(256);
-    if (limit < 2) return 0;
+    c.prime_info.reserve(sizeof(PrimeInfo));
+    PrimeInfo *info = c.prime_info.as<PrimeInfo>();
+    if (limit < 2) {
+        SQF2K_CUDA(cudaMemsetAsync(info, 0, sizeof(PrimeInfo), c.stream));
+        return;
+    }
     uint32_t r = (uint32_t)isqrt_u64(limit);
     if (r < 3) r = 3;
     const uint64_t n_odd = (limit + 1) / 2;  // odd numbers 1..limit (index i <-> 2i+1)
     const uint64_t nseg = ceil_div(n_odd, kSegOdds);
-    // pi(x) < 1.26 x / ln x for x > 1; generous cap
-    const double lx = limit > 16 ? std::log((double)limit) : 2.0;
-    const uint64_t cap = (uint64_t)(1.3 * (double)limit / lx) + 64;
+    if (nseg == 1) {  // small tables: one CTA does everything
+        c.primes_u32.reserve(pi_upper(limit) * 4);
+        launch("primes_small", prime_small_kernel, dim3(1), dim3(kSieveThreads), 0, limit,
+               c.primes_u32.as<uint32_t>(), info);
+        return;
+    }
 
     c.prime_bits.reserve(nseg * kSegWords * 4 + (kMaxBase + 1) * 4);
     c.prime_counts.reserve((nseg + 2) * 4);  // counts[0..nseg] + base-prime count
     c.prime_offsets.reserve((nseg + 1) * 8);
-    c.primes_u32.reserve(cap * 4);
+    c.primes_u32.reserve(pi_upper(limit) * 4);
     uint32_t *bits = c.prime_bits.as<uint32_t>();
     uint32_t *base = bits + nseg * kSegWords;  // tail of the same allocation
     uint32_t *counts = c.prime_counts.as<uint32_t>();
@@ -174,22 +265,29 @@ uint64_t generate_primes_device(uint64_t limit) {
            base, nbase);
     launch("primes_sieve", prime_segment_kernel, dim3((unsigned)nseg), dim3(kSieveThreads), 0,
            limit, (const uint32_t *)base, (const uint32_t *)nbase, bits, counts);
-    // exclusive scan of counts (uint32 in, uint64 out)
+    // exclusive scan of counts (uint32 in, uint64 out); counts[nseg] = 0 puts
+    // the total in offsets[nseg]
     uint64_t *offsets = c.prime_offsets.as<uint64_t>();
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, (int)nseg + 1, c.stream);
-    c.scan_tmp.reserve(tmp_bytes);
-    // counts[nseg] must be 0 for the total to land in offsets[nseg]
+    c.scan_tmp.reserve(std::max<size_t>(tmp_bytes, 64));
     SQF2K_CUDA(cudaMemsetAsync(counts + nseg, 0, 4, c.stream));
     SQF2K_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.ptr, tmp_bytes, counts, offsets,
                                              (int)nseg + 1, c.stream));
     launch("primes_compact", prime_compact_kernel, dim3((unsigned)nseg), dim3(kSieveThreads), 0,
-           (const uint32_t *)bits, (const uint64_t *)offsets, c.primes_u32.as<uint32_t>(), 1);
-    uint64_t total = 0;
-    copy_d2h(&total, offsets + nseg, 8);
+           (const uint32_t *)bits, (const uint64_t *)offsets, c.primes_u32.as<uint32_t>(), 1,
+           offsets + nseg, info);
+}
+
+// Generate every prime <= limit into ctx.primes_u32; returns the count.
+uint64_t generate_primes_device(uint64_t limit) {
+    Context &c = ctx();
+    generate_primes_async(limit);
+    PrimeInfo h;
+    copy_d2h(&h, c.prime_info.ptr, sizeof h);
     SQF2K_CUDA(cudaStreamSynchronize(c.stream));
-    c.primes_count = total + 1;  // + the prime 2
-    return c.primes_count;
+    c.primes_count = h.count;
+    return h.count;
 }
 
 void widen_primes(const uint32_t *in, int64_t *out, uint64_t n) {

@@ -41,10 +41,6 @@ struct ScanParams {
     uint8_t *kvals;      // exponent-dump mode
 };
 
-__device__ __forceinline__ uint32_t lane_of(const uint4 &v, int i) {
-    return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
-}
-
 template <bool EXPO>
 __global__ void __launch_bounds__(kScanThreads) window_scan_kernel(const ScanParams P) {
     __shared__ unsigned long long s_first[65];
@@ -128,17 +124,18 @@ __global__ void __launch_bounds__(kScanThreads) window_scan_kernel(const ScanPar
                 }
         }
     }
-    if (EXPO) return;
+    if (!EXPO) {
 #pragma unroll
-    for (int k = 1; k <= 8; ++k) {
-        uint32_t s = __reduce_add_sync(0xffffffffu, cnt[k]);
-        if ((threadIdx.x & 31) == 0 && s) atomicAdd(&s_hist[k], s);
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < 65; k += blockDim.x) {
-        if (s_hist[k]) atomicAdd(&P.hist[k], (unsigned long long)s_hist[k]);
-        if (s_first[k] != ~0ull)
-            atomicMin(&P.min_n[k], (unsigned long long)(P.first_n + 2 * s_first[k]));
+        for (int k = 1; k <= 8; ++k) {
+            uint32_t s = __reduce_add_sync(0xffffffffu, cnt[k]);
+            if ((threadIdx.x & 31) == 0 && s) atomicAdd(&s_hist[k], s);
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < 65; k += blockDim.x) {
+            if (s_hist[k]) atomicAdd(&P.hist[k], (unsigned long long)s_hist[k]);
+            if (s_first[k] != ~0ull)
+                atomicMin(&P.min_n[k], (unsigned long long)(P.first_n + 2 * s_first[k]));
+        }
     }
 }
 

@@ -5,16 +5,17 @@
 // "not squarefree", search.py:282-286).  Tiles are kTile consecutive slots.
 //
 // Per tile a CTA
-//   1. sets one byte per slot to 1 and stores 0 at every odd multiple of p^2
-//      for the medium primes 11 <= p < kPMed (balanced "items" of <= ~9 hits,
-//      per-CTA incremental offsets, no divisions) and for the bucket primes
-//      p >= kPMed (hit lists precomputed per tile in HBM);
-//   2. packs the bytes into 32-bit LSB-first words, ANDing in the periodic
-//      patterns of p = 3, 5, 7 (q = 9, 25, 49) computed in registers;
-//   3. (fused mode) runs the exponent passes k = 1..k_eff of search.py:368-381
-//      on the packed words, reading n - 2^k from the tile or from the rolled
-//      halo of the previous tile (2^(k_eff-1) slots);
-//      (export mode) stores the packed words to HBM.
+//   1. holds one byte per slot (1 = squarefree so far) and stores 0 at every
+//      odd multiple of p^2 for the medium primes 11 <= p < kPMed (balanced
+//      "items" of <= ~9 hits, per-CTA incremental offsets, no divisions) and
+//      for the bucket primes p >= kPMed (hit lists precomputed per tile in HBM);
+//   2. packs the bytes into 32-bit LSB-first words and ANDs in the periodic
+//      pattern of p = 3, 5, 7 (one table word per u-word mod 9*25*49);
+//   3. fused mode: runs the exponent passes k = 1..k_eff of search.py:368-381
+//      over the packed words -- passes 1..4 unconditionally for every word
+//      (funnel shifts of the word and its left neighbour), the rare remainder
+//      divergently -- reading n - 2^k from the tile or the rolled halo of the
+//      previous tile (2^(k_eff-1) slots); export mode: stores the words.
 //
 // Bytes are laid out so that packing 32 slots is two conflict-free LDS.128
 // and seven shift-or's: within each 1024-slot block, slot s (local) lives at
@@ -25,11 +26,14 @@
 
 #include <stdint.h>
 
+#include <vector>
+
 namespace sqf2k {
 
 constexpr int kTile = 1 << 16;          // slots per tile
 constexpr int kTileWords = kTile / 32;  // 2048 packed words
 constexpr int kThreads = 512;           // CTA size of the tile kernels
+constexpr int kWordsPerThread = kTileWords / kThreads;  // 4
 constexpr int kCtasPerSm = 2;
 constexpr int kDepthMax = 16;           // max exponent resolved in-tile
 constexpr int kHaloMax = 1 << (kDepthMax - 1);
@@ -38,6 +42,31 @@ constexpr uint32_t kPMed = 1024;        // medium primes: 11 <= p < kPMed
 constexpr int kMaxMed = 176;            // pi(1023) - 4 = 168
 constexpr int kMaxItems = 1024;
 constexpr int kItemHits = 8;            // target hits per item per tile
+constexpr uint32_t kPatWords = 9 * 25 * 49;  // period of the p = 3, 5, 7 pattern in words
+constexpr uint32_t kPiBelowPMed = 172;  // pi(1023): table index of the first bucket prime
+constexpr uint32_t kPiSubRoot = 1028;   // pi(8191): last "dense" bucket prime (p^2 < 2^26)
+
+// Bucket primes come in classes j = 0..kClasses-1 of p in [2^(10+j), 2^(11+j)).
+// A class-j work unit is one prime over a sub-range of 2^(22+2j) slots, so it
+// has at most 2^(22+2j) / 2^(20+2j) + 1 = 5 hits: short atomic chains.
+constexpr int kClasses = 22;  // up to p < 2^32
+// pi(2^m) for m = 10..32 (OEIS A007053): class boundaries of a table that
+// holds every prime <= limit.
+__host__ __device__ inline uint32_t pi_pow2(int j) {
+    const uint32_t t[kClasses + 1] = {
+        172u,      309u,      564u,      1028u,     1900u,      3512u,      6542u,     12251u,
+        23000u,    43390u,    82025u,    155611u,   295947u,    564163u,    1077871u,  2063689u,
+        3957809u,  7603553u,  14630843u, 28192750u, 54400028u, 105097565u, 203280221u};
+    return t[j];
+}
+
+// Prime-table split, kept in device memory so no host sync is needed.
+struct PrimeInfo {
+    unsigned long long count;  // primes in the table
+    uint32_t i_lo;             // first bucket prime (p >= kPMed)
+    uint32_t i_hi;             // end of the bucket primes (p^2 <= n_max)
+    uint32_t cls[kClasses + 1];  // index of the first prime >= 2^(10+j), clipped to count
+};
 
 struct TileParams {
     int64_t base_n;      // n(u) = base_n + 2u
@@ -49,13 +78,11 @@ struct TileParams {
     uint32_t n_tiles;
     uint32_t k_eff;      // passes inside the tile
     uint32_t k_max;      // run limit: escalate when k_max > k_eff
-    uint32_t pat_q[3];   // 9, 25, 49 (1 when that prime is absent)
-    uint32_t pat_bits[3];
-    uint32_t pat_r[3];   // residue of the first hit slot
     uint32_t n_med;
     uint32_t n_items;
-    const uint32_t *med;    // per medium prime: q, residue, kTile mod q   (3 x n_med)
-    const uint32_t *items;  // per item: (med << 16 | j), stride          (2 x n_items)
+    const uint32_t *pattern;     // kPatWords words of the p = 3, 5, 7 mask, by u-word
+    const uint32_t *med;         // per medium prime: q, kTile mod q          (2 x n_med)
+    const uint32_t *items;       // per item: (med << 16 | j), stride          (2 x n_items)
     const uint32_t *tile_start;  // bucket hit list bounds, n_tiles + 1
     const uint16_t *hits;        // bucket hits, offsets within the tile
     unsigned long long *hist;    // [65]
@@ -70,18 +97,37 @@ struct TileParams {
 };
 
 __device__ __forceinline__ uint32_t byte_pos(uint32_t s) {
-    return (s & ~1023u) | ((s >> 3) & 3u) | ((s & 3u) << 2) | (((s >> 5) & 31u) << 4) |
-           (((s >> 2) & 1u) << 9);
+    return (s & ~1023u) | ((s >> 3) & 3u) | ((s & 3u) << 2) | ((s >> 1) & 0x1f0u) |
+           ((s << 7) & 0x200u);
 }
 
-// shift left with PTX clamping: amounts >= 32 give 0
-__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t s) {
-    uint32_t r;
-    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
-    return r;
+// residue of the first slot u >= 0 with q | base_n + 2u, i.e. u = -base_n/2 mod q
+__device__ __host__ __forceinline__ uint64_t slot_residue(int64_t base_n, uint64_t q) {
+    uint64_t a;
+    if (base_n >= 0) {
+        uint64_t t = (uint64_t)base_n % q;
+        a = t ? q - t : 0;
+    } else {
+        a = ((uint64_t)(-base_n)) % q;
+    }
+    return (a & 1) ? (a + q) / 2 : a / 2;
 }
 
-// x mod q for the CTA-uniform 64-bit position u (q < 2^32)
-__device__ __forceinline__ uint32_t mod_u64(uint64_t u, uint32_t q) { return (uint32_t)(u % q); }
+// Host description of one batch domain for run_tile_batch (tile.cu).
+struct BatchArgs {
+    bool fused;
+    int64_t base_n;
+    uint64_t U, scan_lo, z, one_u;
+    uint32_t H, k_eff, k_max;
+    const uint32_t *primes;       // device table
+    const PrimeInfo *info;        // device split
+    uint64_t n_primes_bound;      // host upper bound of the table size
+    uint32_t pattern_present;     // bit i: prime 3/5/7 in the table
+    const std::vector<uint32_t> *med_primes;
+    unsigned long long *hist, *min_n, *esc, *esc_count, *fail, *fail_count;
+    uint64_t esc_cap, fail_cap;
+    uint32_t *bits_out;
+};
+void run_tile_batch(const BatchArgs &a);
 
 }  // namespace sqf2k
