@@ -83,7 +83,13 @@ typedef struct sqf2k_verify_opts {
                               exact trial-division kernel.  Tests force tiny
                               depths to exercise escalation.                   */
     uint64_t batch_slots;  /* odd slots per device batch; 0 = default 2^36     */
+    uint32_t flags;        /* SQF2K_EXACT_BUCKETS: exact (count + scan) large-
+                              prime lists from the start instead of the fixed-
+                              capacity lists with exact fallback (tests)      */
+    uint32_t reserved;
 } sqf2k_verify_opts_t;
+
+#define SQF2K_EXACT_BUCKETS 1u
 
 /* Per-kernel device-time statistics (CUDA events on the library's stream). */
 typedef struct sqf2k_kstat {

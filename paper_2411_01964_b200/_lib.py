@@ -46,7 +46,12 @@ class VerifyOpts(ctypes.Structure):
         ("pipeline", ctypes.c_uint32),
         ("tile_depth", ctypes.c_uint32),
         ("batch_slots", ctypes.c_uint64),
+        ("flags", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
     ]
+
+
+EXACT_BUCKETS = 1
 
 
 class KStat(ctypes.Structure):

@@ -40,16 +40,18 @@ __global__ void __launch_bounds__(kSieveThreads) prime_small_kernel(uint64_t lim
     __shared__ uint32_t base[128];
     __shared__ uint32_t nbase;
     const uint32_t r = (uint32_t)isqrt_u64(limit);  // <= 362
-    if (threadIdx.x == 0) {
-        __shared__ uint8_t comp[400];
+    if (threadIdx.x < 32) {
+        // odd base primes <= r by trial division, ordered by a warp ballot
         uint32_t nb = 0;
-        for (uint32_t i = 0; i <= r && i < 400; ++i) comp[i] = 0;
-        for (uint32_t p = 3; p <= r; p += 2) {
-            if (comp[p]) continue;
-            base[nb++] = p;
-            for (uint32_t m = p * p; m <= r; m += 2 * p) comp[m] = 1;
+        for (uint32_t c0 = 3; c0 <= r; c0 += 64) {
+            const uint32_t cand = c0 + 2 * threadIdx.x;
+            bool prime = cand <= r;
+            for (uint32_t d = 3; prime && d * d <= cand; d += 2) prime = cand % d != 0;
+            const uint32_t bal = __ballot_sync(0xffffffffu, prime);
+            if (prime) base[nb + __popc(bal & ((1u << threadIdx.x) - 1u))] = cand;
+            nb += __popc(bal);
         }
-        nbase = nb;
+        if (threadIdx.x == 0) nbase = nb;
     }
     for (int j = threadIdx.x; j < kSegWords; j += blockDim.x) {
         const uint64_t m0 = 1 + 64ull * j;  // odd numbers 2i+1, i = 32j..32j+31
@@ -63,9 +65,10 @@ __global__ void __launch_bounds__(kSieveThreads) prime_small_kernel(uint64_t lim
         w[j] = word;
     }
     __syncthreads();
+    const uint32_t n_idx = (uint32_t)((limit + 1) / 2);  // odd numbers <= limit
     for (uint32_t k = 0; k < nbase; ++k) {
         const uint32_t p = base[k];
-        for (uint32_t i = (p * p - 1) / 2 + threadIdx.x * p; i < (uint32_t)kSegOdds; i += blockDim.x * p)
+        for (uint32_t i = (p * p - 1) / 2 + threadIdx.x * p; i < n_idx; i += blockDim.x * p)
             atomicAnd(&w[i >> 5], ~(1u << (i & 31)));
     }
     __syncthreads();

@@ -3,7 +3,6 @@
 // min-k scan, or sieve export).  No host synchronisation inside a batch.
 #include <algorithm>
 #include <cstring>
-#include <map>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -42,50 +41,78 @@ __global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__res
 // -------------------------------------------------------------------------
 // Bucket pass: every hit u of a bucket prime (p >= kPMed, p^2 <= n_max) in the
 // batch domain [0, U), as a 16-bit offset in the list of tile u >> 16.
-// Work units are (prime, sub-range) pairs of <= 5 hits (see kClasses).
-// FILL places hit i of tile t at offsets[t] + (--counts[t]): the count pass
-// leaves counts[t] = size, the fill pass brings it back to 0.
-template <bool FILL>
+// Work units are (prime, sub-range) pairs of <= 5 hits (see kClasses), one
+// flat index space over all classes so each thread runs one short chain.
+//   MODE 0 (fixed): hit i of tile t goes to hits[t * kBucketCap + i]; counts
+//          beyond the capacity raise *overflow (the batch is then redone in
+//          exact mode).
+//   MODE 1 (count) / MODE 2 (fill): exact lists after an exclusive scan of
+//          the counts; the fill places hits at offsets[t] + (--counts[t]).
+template <int MODE>
 __global__ void __launch_bounds__(256) bucket_kernel(
     const uint32_t *__restrict__ primes, const PrimeInfo *__restrict__ info, int64_t base_n,
     uint64_t U, uint32_t *__restrict__ counts, const uint32_t *__restrict__ offsets,
-    uint16_t *__restrict__ hits) {
-    const uint32_t i_hi = info->i_hi;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (int j = 0; j < kClasses; ++j) {
-        const uint32_t p_lo = max(info->cls[j], info->i_lo);
-        const uint32_t p_hi = min(info->cls[j + 1], i_hi);
-        if (p_lo >= p_hi) continue;
+    uint16_t *__restrict__ hits, unsigned int *__restrict__ overflow) {
+    __shared__ unsigned long long s_end[kClasses];  // cumulative work per class
+    __shared__ uint32_t s_lo[kClasses];
+    __shared__ unsigned long long s_nsub[kClasses];
+    if (threadIdx.x == 0) {
+        unsigned long long acc = 0;
+        const uint32_t i_lo = info->i_lo, i_hi = info->i_hi;
+        for (int j = 0; j < kClasses; ++j) {
+            const uint32_t p_lo = max(info->cls[j], i_lo), p_hi = min(info->cls[j + 1], i_hi);
+            const int sh = min(22 + 2 * j, 62);
+            const unsigned long long n_sub = (U + (1ull << sh) - 1) >> sh;
+            s_lo[j] = p_lo;
+            s_nsub[j] = n_sub;
+            acc += p_lo < p_hi ? (unsigned long long)(p_hi - p_lo) * n_sub : 0ull;
+            s_end[j] = acc;
+        }
+    }
+    __syncthreads();
+    const unsigned long long n_work = s_end[kClasses - 1];
+    for (unsigned long long w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < n_work;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        int j = 0;
+        while (w >= s_end[j]) ++j;
+        const unsigned long long local = w - (j ? s_end[j - 1] : 0ull);
+        const unsigned long long n_sub = s_nsub[j];
         const int sh = min(22 + 2 * j, 62);
-        const uint64_t n_sub = (U + (1ull << sh) - 1) >> sh;
-        const uint64_t n_work = (uint64_t)(p_hi - p_lo) * n_sub;
-        for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < n_work; w += stride) {
-            const uint64_t p = primes[p_lo + w / n_sub];
-            const uint64_t lo = (w % n_sub) << sh;
-            const uint64_t hi = lo + (1ull << sh) < U ? lo + (1ull << sh) : U;
-            const uint64_t q = p * p;
-            const uint64_t r = slot_residue(base_n, q);
-            const uint64_t lm = lo % q;
-            for (uint64_t u = lo + (r >= lm ? r - lm : r + q - lm); u < hi; u += q) {
-                const uint32_t t = (uint32_t)(u >> 16);
-                if (FILL) {
-                    const uint32_t pos = offsets[t] + atomicSub(&counts[t], 1u) - 1u;
-                    hits[pos] = (uint16_t)(u & 0xffff);
-                } else {
-                    atomicAdd(&counts[t], 1u);
-                }
+        const uint64_t p = primes[s_lo[j] + local / n_sub];
+        const uint64_t lo = (uint64_t)(local % n_sub) << sh;
+        const uint64_t hi = lo + (1ull << sh) < U ? lo + (1ull << sh) : U;
+        const uint64_t q = p * p;
+        const uint64_t r = slot_residue(base_n, q);
+        const uint64_t lm = lo % q;
+        for (uint64_t u = lo + (r >= lm ? r - lm : r + q - lm); u < hi; u += q) {
+            const uint32_t t = (uint32_t)(u >> 16);
+            if (MODE == 0) {
+                const uint32_t pos = atomicAdd(&counts[t], 1u);
+                if (pos < (uint32_t)kBucketCap)
+                    hits[(uint64_t)t * kBucketCap + pos] = (uint16_t)(u & 0xffff);
+                else
+                    atomicOr(overflow, 1u);
+            } else if (MODE == 1) {
+                atomicAdd(&counts[t], 1u);
+            } else {
+                const uint32_t pos = offsets[t] + atomicSub(&counts[t], 1u) - 1u;
+                hits[pos] = (uint16_t)(u & 0xffff);
             }
         }
     }
 }
 
 // -------------------------------------------------------------------------
+// Shared memory of a tile CTA.  The packed words live in a 2-tile ring:
+// tile t occupies half (t & 1), and its halo (the previous tile's last
+// 2^(k_eff-1) slots) is the tail of the other half -- no copy per tile.
+constexpr int kRingWords = 2 * kTileWords;  // 4096 (power of two)
 struct TileSmem {
-    uint8_t bytes[kTile];                       // 64 KB, 16-byte aligned
-    uint32_t bits[kHaloWordsMax + kTileWords];  // halo + tile (12 KB)
+    uint8_t bytes[kTile];        // 64 KB, 16-byte aligned
+    uint32_t ring[kRingWords];   // 16 KB
     uint32_t med_q[kMaxMed], med_tq[kMaxMed], off[kMaxMed];
     unsigned long long first[kDepthMax + 1];
-    uint32_t cnt[kDepthMax + 1];                // counts of k >= 5 (rare)
+    uint32_t cnt[kDepthMax + 1];  // counts of k >= 5 (rare)
     uint32_t need;
 };
 
@@ -95,17 +122,32 @@ __device__ __forceinline__ void init_bytes(uint8_t *bytes, uint32_t len) {
         reinterpret_cast<uint4 *>(bytes)[i] = one;
 }
 
-// clear the medium-prime hits in [0, len) of the current base
+__device__ __forceinline__ void init_tile_bytes(uint8_t *bytes) {
+    const uint4 one = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+#pragma unroll
+    for (int r = 0; r < kTile / 16 / kThreads; ++r)
+        reinterpret_cast<uint4 *>(bytes)[threadIdx.x + r * kThreads] = one;
+}
+
+// Clear the medium-prime hits in [0, len) of the current base.  Work comes
+// as warp tasks of 32 lane descriptors (m | mult << 8, step): lane clears
+// off[m] + mult*q[m], then every `step` slots -- a whole warp sweeping one
+// small prime (steps 32*S*q) or 32 independent items of larger primes.  The
+// host sorts descriptors by trip count and balances tasks over the warps.
 __device__ __forceinline__ void scatter_medium(uint8_t *bytes, const uint32_t *off,
-                                               const uint32_t *med_q, const TileParams &P,
-                                               uint32_t len) {
-    for (uint32_t it = threadIdx.x; it < P.n_items; it += kThreads) {
-        const uint32_t mj = __ldg(&P.items[2 * it]), stride = __ldg(&P.items[2 * it + 1]);
-        const uint32_t m = mj >> 16;
-        uint32_t o = off[m] + (mj & 0xffffu) * med_q[m];
-        for (; o + stride < len; o += 2 * stride) {
+                                               const uint32_t *med_q, const uint2 *tasks,
+                                               const uint32_t *task_beg, uint32_t len) {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t k1 = __ldg(&task_beg[warp + 1]);
+    for (uint32_t tk = __ldg(&task_beg[warp]); tk < k1; ++tk) {
+        const uint2 d = __ldg(&tasks[tk * 32 + lane]);
+        if (!d.y) continue;
+        const uint32_t m = d.x & 0xffu;
+        uint32_t o = off[m] + (d.x >> 8) * med_q[m];
+        const uint32_t step = d.y;
+        for (; o + step < len; o += 2 * step) {
             bytes[byte_pos(o)] = 0;
-            bytes[byte_pos(o + stride)] = 0;
+            bytes[byte_pos(o + step)] = 0;
         }
         if (o < len) bytes[byte_pos(o)] = 0;
     }
@@ -114,8 +156,16 @@ __device__ __forceinline__ void scatter_medium(uint8_t *bytes, const uint32_t *o
 // clear the bucket hits of tile t with offsets in [skip, kTile), shifted by -skip
 __device__ __forceinline__ void scatter_bucket(uint8_t *bytes, const TileParams &P, uint32_t t,
                                                uint32_t skip) {
-    const uint32_t b = __ldg(&P.tile_start[t]), e = __ldg(&P.tile_start[t + 1]);
-    for (uint32_t i = b + threadIdx.x; i < e; i += kThreads) {
+    uint32_t b, e;
+    if (P.tile_start) {
+        b = __ldg(&P.tile_start[t]);
+        e = __ldg(&P.tile_start[t + 1]);
+    } else {
+        b = t * (uint32_t)kBucketCap;
+        e = b + min(__ldg(&P.tile_count[t]), (uint32_t)kBucketCap);
+    }
+    // last threads first: the task balance leaves them no lighter than others
+    for (uint32_t i = b + (kThreads - 1 - threadIdx.x); i < e; i += kThreads) {
         const uint32_t o = __ldg(&P.hits[i]);
         if (o >= skip) bytes[byte_pos(o - skip)] = 0;
     }
@@ -130,11 +180,12 @@ __device__ __forceinline__ void advance_offsets(uint32_t *off, const uint32_t *m
     }
 }
 
-// Pack WORDS words of bytes (domain slot `base`) into out[].  pbase is
-// (base / 32) mod kPatWords.  EDGE applies the n < 1 zero region and the end.
-template <int WORDS, bool EDGE>
-__device__ __forceinline__ void pack_words(const uint8_t *bytes, uint32_t *out, uint64_t base,
-                                           uint32_t pbase, const TileParams &P) {
+// Pack WORDS words of bytes (domain slot `base`) into ring[(at + w) & mask].
+// pbase is (base / 32) mod kPatWords.  EDGE applies the n < 1 zero region
+// and the domain end.
+template <int WORDS, bool EDGE, bool WRAP = true>
+__device__ __forceinline__ void pack_words(const uint8_t *bytes, uint32_t *ring, uint32_t at,
+                                           uint64_t base, uint32_t pbase, const TileParams &P) {
 #pragma unroll
     for (int r = 0; r < (WORDS + kThreads - 1) / kThreads; ++r) {
         const uint32_t w = threadIdx.x + r * kThreads;
@@ -154,18 +205,19 @@ __device__ __forceinline__ void pack_words(const uint8_t *bytes, uint32_t *out, 
             if (u0 < P.z) word = (u0 + 32 <= P.z) ? 0u : (word & (~0u << (uint32_t)(P.z - u0)));
             if (u0 + 32 > P.U) word = (u0 >= P.U) ? 0u : (word & ((1u << (uint32_t)(P.U - u0)) - 1u));
         }
-        out[w] = word;
+        ring[WRAP ? ((at + w) & (kRingWords - 1)) : at + w] = word;
     }
 }
 
 // The pre-tile packs H = HW*32 slots (HW in {32, 64, ..., 1024}).
-__device__ __forceinline__ void pack_halo(const uint8_t *bytes, uint32_t *out, uint32_t HW,
-                                          uint64_t base, uint32_t pbase, const TileParams &P) {
-    if (HW > 512) pack_words<kHaloWordsMax, true>(bytes, out, base, pbase, P);
-    else if (HW > 256) pack_words<512, true>(bytes, out, base, pbase, P);
-    else if (HW > 128) pack_words<256, true>(bytes, out, base, pbase, P);
-    else if (HW > 64) pack_words<128, true>(bytes, out, base, pbase, P);
-    else pack_words<64, true>(bytes, out, base, pbase, P);
+__device__ __forceinline__ void pack_halo(const uint8_t *bytes, uint32_t *ring, uint32_t at,
+                                          uint32_t HW, uint64_t base, uint32_t pbase,
+                                          const TileParams &P) {
+    if (HW > 512) pack_words<kHaloWordsMax, true>(bytes, ring, at, base, pbase, P);
+    else if (HW > 256) pack_words<512, true>(bytes, ring, at, base, pbase, P);
+    else if (HW > 128) pack_words<256, true>(bytes, ring, at, base, pbase, P);
+    else if (HW > 64) pack_words<128, true>(bytes, ring, at, base, pbase, P);
+    else pack_words<64, true>(bytes, ring, at, base, pbase, P);
 }
 
 __device__ __forceinline__ void append(unsigned long long *list, unsigned long long *count,
@@ -174,15 +226,29 @@ __device__ __forceinline__ void append(unsigned long long *list, unsigned long l
     if (i < cap) list[i] = n;
 }
 
-// passes k >= 5 for one word (divergent, rare), then escalation / failure
-__device__ __forceinline__ void scan_residue(TileSmem &S, const TileParams &P, uint32_t HW,
-                                          uint32_t w, uint64_t u0, uint32_t pend, uint32_t need) {
-    const uint32_t cur = S.bits[HW + w], prv = S.bits[HW + w - 1];
-    for (uint32_t k = 5; k <= P.k_eff && pend; ++k) {
+// Leftover slots of one word after the in-tile passes: escalation (k_max >
+// k_eff) or failures.  Out of line: it essentially never runs.
+__device__ __noinline__ void spill_word(uint32_t pend, uint64_t u0, int64_t base_n,
+                                        unsigned long long *list, unsigned long long *count,
+                                        uint64_t cap) {
+    for (uint32_t x = pend; x; x &= x - 1)
+        append(list, count, cap, (uint64_t)(base_n + 2 * (int64_t)(u0 + __ffs(x) - 1)));
+}
+
+// Passes k = 5..k_eff for one word (divergent, rare: ~0.4% of words).
+__device__ __noinline__ void scan_residue(TileSmem &S, uint32_t hb, uint32_t w, uint64_t u0,
+                                          uint32_t pend, uint32_t need, uint32_t k_eff,
+                                          uint32_t k_max, int64_t base_n, unsigned long long *esc,
+                                          unsigned long long *esc_count, uint64_t esc_cap,
+                                          unsigned long long *fail,
+                                          unsigned long long *fail_count, uint64_t fail_cap) {
+    const uint32_t cur = S.ring[(hb + w) & (kRingWords - 1)];
+    const uint32_t prv = S.ring[(hb + w - 1) & (kRingWords - 1)];
+    for (uint32_t k = 5; k <= k_eff && pend; ++k) {
         uint32_t sl;
         if (k == 5) sl = __funnelshift_l(prv, cur, 16);
         else if (k == 6) sl = prv;
-        else sl = S.bits[HW + w - (1u << (k - 6))];
+        else sl = S.ring[(hb + w - (1u << (k - 6))) & (kRingWords - 1)];
         const uint32_t nw = pend & sl;
         if (nw) {
             atomicAdd(&S.cnt[k], (uint32_t)__popc(nw));
@@ -191,12 +257,8 @@ __device__ __forceinline__ void scan_residue(TileSmem &S, const TileParams &P, u
         pend &= ~sl;
     }
     if (pend) {
-        const bool esc = P.k_max > P.k_eff;
-        for (uint32_t x = pend; x; x &= x - 1) {
-            const uint64_t n = (uint64_t)(P.base_n + 2 * (int64_t)(u0 + __ffs(x) - 1));
-            if (esc) append(P.esc, P.esc_count, P.esc_cap, n);
-            else append(P.fail, P.fail_count, P.fail_cap, n);
-        }
+        if (k_max > k_eff) spill_word(pend, u0, base_n, esc, esc_count, esc_cap);
+        else spill_word(pend, u0, base_n, fail, fail_count, fail_cap);
     }
 }
 
@@ -211,12 +273,15 @@ __device__ __forceinline__ void pass(uint32_t &pend, uint32_t sl, uint32_t &cnt,
     pend &= ~sl;
 }
 
-// Exponent passes over the tile's words.  EDGE masks the scan range, TRACK
-// records per-k least slots while this CTA still lacks them, KMAIN is the
-// number of unconditional passes (4, or k_eff when smaller).
+// Exponent passes over the tile's words (ring half starting at hb).  EDGE
+// masks the scan range, TRACK records per-k least slots while this CTA still
+// lacks them, KMAIN is the number of unconditional passes (4, or k_eff).
+// Words left pending after pass 4 (~0.4%) finish in one divergent loop per
+// warp after all of the thread's words.
 template <bool EDGE, bool TRACK, int KMAIN>
-__device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint32_t HW,
+__device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint32_t hb,
                                           uint64_t tb, uint32_t need, uint32_t (&c)[5]) {
+    uint32_t left[kWordsPerThread];
 #pragma unroll
     for (int r = 0; r < kWordsPerThread; ++r) {
         const uint32_t w = threadIdx.x + r * kThreads;
@@ -231,37 +296,43 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
                 if (P.one_u >= u0 && P.one_u < u0 + 32) pend &= ~(1u << (uint32_t)(P.one_u - u0));
             }
         }
-        const uint32_t cur = S.bits[HW + w], prv = S.bits[HW + w - 1];
+        const uint32_t cur = S.ring[hb + w];
+        const uint32_t prv = S.ring[(hb + w - 1) & (kRingWords - 1)];
         pass<TRACK>(pend, __funnelshift_l(prv, cur, 1), c[1], 1, need, u0, S);
         if (KMAIN >= 2) pass<TRACK>(pend, __funnelshift_l(prv, cur, 2), c[2], 2, need, u0, S);
         if (KMAIN >= 3) pass<TRACK>(pend, __funnelshift_l(prv, cur, 4), c[3], 3, need, u0, S);
         if (KMAIN >= 4) pass<TRACK>(pend, __funnelshift_l(prv, cur, 8), c[4], 4, need, u0, S);
-        if (pend) {
+        left[r] = pend;
+    }
+    if (__any_sync(0xffffffffu, left[0] | left[1] | left[2] | left[3])) {
+#pragma unroll
+        for (int r = 0; r < kWordsPerThread; ++r) {
+            if (!left[r]) continue;
+            const uint32_t w = threadIdx.x + r * kThreads;
+            const uint64_t u0 = tb + 32ull * w;
             if (KMAIN == 4) {
-                scan_residue(S, P, HW, w, u0, pend, need);
-            } else {  // k_eff = KMAIN < 4: leftovers are final
-                const bool esc = P.k_max > P.k_eff;
-                for (uint32_t x = pend; x; x &= x - 1) {
-                    const uint64_t n = (uint64_t)(P.base_n + 2 * (int64_t)(u0 + __ffs(x) - 1));
-                    if (esc) append(P.esc, P.esc_count, P.esc_cap, n);
-                    else append(P.fail, P.fail_count, P.fail_cap, n);
-                }
+                scan_residue(S, hb, w, u0, left[r], need, P.k_eff, P.k_max, P.base_n, P.esc,
+                             P.esc_count, P.esc_cap, P.fail, P.fail_count, P.fail_cap);
+            } else if (P.k_max > P.k_eff) {  // k_eff = KMAIN < 4: leftovers leave the tile
+                spill_word(left[r], u0, P.base_n, P.esc, P.esc_count, P.esc_cap);
+            } else {
+                spill_word(left[r], u0, P.base_n, P.fail, P.fail_count, P.fail_cap);
             }
         }
     }
 }
 
 template <int KMAIN>
-__device__ __forceinline__ void scan_dispatch(TileSmem &S, const TileParams &P, uint32_t HW,
+__device__ __forceinline__ void scan_dispatch(TileSmem &S, const TileParams &P, uint32_t hb,
                                               uint64_t tb, bool edge, uint32_t need,
                                               uint32_t (&c)[5]) {
     const bool track = (need & 0x1eu) != 0;
     if (edge) {
-        if (track) scan_tile<true, true, KMAIN>(S, P, HW, tb, need, c);
-        else scan_tile<true, false, KMAIN>(S, P, HW, tb, need, c);
+        if (track) scan_tile<true, true, KMAIN>(S, P, hb, tb, need, c);
+        else scan_tile<true, false, KMAIN>(S, P, hb, tb, need, c);
     } else {
-        if (track) scan_tile<false, true, KMAIN>(S, P, HW, tb, need, c);
-        else scan_tile<false, false, KMAIN>(S, P, HW, tb, need, c);
+        if (track) scan_tile<false, true, KMAIN>(S, P, hb, tb, need, c);
+        else scan_tile<false, false, KMAIN>(S, P, hb, tb, need, c);
     }
 }
 
@@ -296,13 +367,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     init_bytes(S.bytes, pre ? H : (uint32_t)kTile);
     __syncthreads();
 
+    // ring half of tile t0 and the halo just below it
+    const uint32_t hb0 = (t0 & 1u) * kTileWords;
     if (FUSED) {
         if (pre) {
             // pre-tile: sieve the H slots below the chunk into the halo words
-            scatter_medium(S.bytes, S.off, S.med_q, P, H);
+            scatter_medium(S.bytes, S.off, S.med_q, P.tasks, P.task_beg, H);
             scatter_bucket(S.bytes, P, t0 - 1, kTile - H);
             __syncthreads();
-            pack_halo(S.bytes, S.bits, HW, b0, pbase, P);
+            pack_halo(S.bytes, S.ring, hb0 + kRingWords - HW, HW, b0, pbase, P);
             for (uint32_t m = threadIdx.x; m < P.n_med; m += kThreads) {
                 const uint32_t o = S.off[m] - H % S.med_q[m];
                 S.off[m] = min(o, o + S.med_q[m]);
@@ -312,7 +385,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             __syncthreads();
             init_bytes(S.bytes, kTile);
         } else {
-            for (uint32_t i = threadIdx.x; i < HW; i += kThreads) S.bits[i] = 0u;
+            for (uint32_t i = threadIdx.x; i < HW; i += kThreads)
+                S.ring[(hb0 + kRingWords - HW + i) & (kRingWords - 1)] = 0u;
         }
         __syncthreads();
     }
@@ -321,19 +395,22 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     const uint32_t kmain = P.k_eff < 4 ? P.k_eff : 4;
     for (uint32_t t = t0; t < t1; ++t) {
         const uint64_t tb = (uint64_t)t * kTile;
-        scatter_medium(S.bytes, S.off, S.med_q, P, kTile);
+        const uint32_t hb = (t & 1u) * kTileWords;
+#ifndef SQF2K_EXP_NO_SCATTER
+        scatter_medium(S.bytes, S.off, S.med_q, P.tasks, P.task_beg, kTile);
         scatter_bucket(S.bytes, P, t, 0);
+#endif
         __syncthreads();
         const bool edge_pack = tb < P.z || tb + kTile > P.U;
-        if (edge_pack) pack_words<kTileWords, true>(S.bytes, S.bits + HW, tb, pbase, P);
-        else pack_words<kTileWords, false>(S.bytes, S.bits + HW, tb, pbase, P);
+        if (edge_pack) pack_words<kTileWords, true, false>(S.bytes, S.ring, hb, tb, pbase, P);
+        else pack_words<kTileWords, false, false>(S.bytes, S.ring, hb, tb, pbase, P);
         advance_offsets(S.off, S.med_q, S.med_tq, P.n_med);
         pbase += kTileWords;
         if (pbase >= kPatWords) pbase -= kPatWords;
         __syncthreads();
         if (!FUSED) {
             for (uint32_t w = threadIdx.x; w < kTileWords; w += kThreads)
-                P.bits_out[(uint64_t)t * kTileWords + w] = S.bits[w];
+                P.bits_out[(uint64_t)t * kTileWords + w] = S.ring[hb + w];
             init_bytes(S.bytes, kTile);
             __syncthreads();
             continue;
@@ -342,14 +419,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         const uint32_t need = S.need;
         const bool edge = tb < P.scan_lo || tb + kTile > P.U ||
                           (P.one_u >= tb && P.one_u < tb + kTile);
+#ifndef SQF2K_EXP_NO_SCAN
         switch (kmain) {
-            case 1: scan_dispatch<1>(S, P, HW, tb, edge, need, c); break;
-            case 2: scan_dispatch<2>(S, P, HW, tb, edge, need, c); break;
-            case 3: scan_dispatch<3>(S, P, HW, tb, edge, need, c); break;
-            default: scan_dispatch<4>(S, P, HW, tb, edge, need, c); break;
+            case 1: scan_dispatch<1>(S, P, hb, tb, edge, need, c); break;
+            case 2: scan_dispatch<2>(S, P, hb, tb, edge, need, c); break;
+            case 3: scan_dispatch<3>(S, P, hb, tb, edge, need, c); break;
+            default: scan_dispatch<4>(S, P, hb, tb, edge, need, c); break;
         }
-        if (t + 1 < t1) init_bytes(S.bytes, kTile);  // the next tile's bytes
+#endif
+        if (t + 1 < t1) init_tile_bytes(S.bytes);  // the next tile's bytes
         __syncthreads();
+        // per-k least n of this CTA: the first tile where k shows up wins
         if (threadIdx.x >= 1 && threadIdx.x <= kDepthMax) {
             const unsigned long long f = S.first[threadIdx.x];
             if (f != ~0ull) {
@@ -358,9 +438,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                 S.first[threadIdx.x] = ~0ull;
             }
         }
-        // roll the halo: the last H slots of this tile precede the next one
-        for (uint32_t i = threadIdx.x; i < HW; i += kThreads) S.bits[i] = S.bits[kTileWords + i];
-        // (the next tile's scatter touches only bytes; its pack follows a barrier)
+        // the next tile's scatter touches only bytes; its pack (which writes
+        // the ring half holding this tile's halo source) follows a barrier
     }
 
     if (FUSED) {
@@ -377,34 +456,76 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
 }
 
 // -------------------------------------------------------------------------
-// Medium-prime tables (q, kTile mod q) and balanced items, built on the host
-// from the table's primes in [11, kPMed) and cached on the device per set.
+// Medium-prime tables (q, kTile mod q) and the scatter tasks, built on the
+// host from the table's primes in [11, kPMed) and cached on the device per
+// set.  A prime with h = kTile/q hits per tile and h >= 16 is swept by whole
+// warps (S sweeps of ~kItemHits hits per lane: lane l starts at hit l + 32s,
+// step 32*S*q); a rarer prime is split into ~kItemHits-hit items (start j,
+// step parts*q).  Descriptors sorted by trip count fill 32-lane tasks, and the
+// tasks go to the kThreads/32 warps longest-first.
 struct MedTables {
-    std::vector<uint32_t> med, items;
-    uint32_t n_med = 0, n_items = 0;
+    std::vector<uint32_t> med;
+    std::vector<uint32_t> tasks;  // (x, y) pairs, 32 per task, ordered by warp
+    std::vector<uint32_t> beg;    // warp w runs tasks [beg[w], beg[w+1])
+    uint32_t n_med = 0, n_tasks = 0;
 };
 
 MedTables build_med(const std::vector<uint32_t> &med_primes) {
     MedTables t;
+    struct Desc {
+        double trips;
+        uint32_t x, y;
+    };
+    std::vector<Desc> descs;
     for (uint32_t p : med_primes) {
         if (t.n_med >= (uint32_t)kMaxMed) break;
-        const uint32_t q = p * p;
+        const uint32_t q = p * p, m = t.n_med;
         t.med.push_back(q);
         t.med.push_back((uint32_t)kTile % q);
-        uint32_t m = (uint32_t)kTile / (q * (uint32_t)kItemHits);
-        m = std::max<uint32_t>(1, std::min<uint32_t>(m, 64));
-        for (uint32_t j = 0; j < m && t.n_items < (uint32_t)kMaxItems; ++j, ++t.n_items) {
-            t.items.push_back((t.n_med << 16) | j);
-            t.items.push_back(m * q);
+        const double h = (double)kTile / q;
+        if (h >= 16.0) {
+            uint32_t S = (uint32_t)(h / (32.0 * kItemHits) + 0.5);
+            S = std::max<uint32_t>(1, S);
+            for (uint32_t sw = 0; sw < S; ++sw)
+                for (uint32_t l = 0; l < 32; ++l)
+                    descs.push_back({h / (32.0 * S) + 1.0, m | ((l + 32 * sw) << 8), 32 * S * q});
+        } else {
+            uint32_t parts = std::max<uint32_t>(1, (uint32_t)(h / kItemHits + 0.5));
+            for (uint32_t j = 0; j < parts; ++j)
+                descs.push_back({h / parts + 1.0, m | (j << 8), parts * q});
         }
         ++t.n_med;
     }
+    std::stable_sort(descs.begin(), descs.end(),
+                     [](const Desc &a, const Desc &b) { return a.trips > b.trips; });
+    const uint32_t n_tasks = (uint32_t)((descs.size() + 31) / 32);
+    std::vector<double> cost(n_tasks, 0.0);
+    for (uint32_t k = 0; k < n_tasks; ++k) cost[k] = descs[32 * k].trips + 1.0;  // + task overhead
+    constexpr int kWarps = kThreads / 32;
+    std::vector<double> load(kWarps, 0.0);
+    std::vector<std::vector<uint32_t>> per_warp(kWarps);
+    for (uint32_t k = 0; k < n_tasks; ++k) {  // tasks are already longest-first
+        const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        load[w] += cost[k];
+        per_warp[w].push_back(k);
+    }
+    t.beg.push_back(0);
+    for (int w = 0; w < kWarps; ++w) {
+        for (uint32_t k : per_warp[w])
+            for (uint32_t l = 0; l < 32; ++l) {
+                const uint32_t i = 32 * k + l;
+                t.tasks.push_back(i < descs.size() ? descs[i].x : 0u);
+                t.tasks.push_back(i < descs.size() ? descs[i].y : 0u);  // step 0: idle lane
+            }
+        t.beg.push_back((uint32_t)(t.tasks.size() / 64));
+    }
+    t.n_tasks = n_tasks;
     return t;
 }
 
 struct MedCache {
     std::vector<uint32_t> key;
-    uint32_t n_med = 0, n_items = 0;
+    uint32_t n_med = 0, n_tasks = 0;
     DevBuf buf;
 };
 
@@ -430,21 +551,24 @@ size_t tile_smem_bytes() { return sizeof(TileSmem); }
 // of (U/p^2 + 1) <= U / (2 * 1029) + n_bucket_primes.
 uint64_t bucket_hits_bound(uint64_t U, uint64_t n_bucket) { return U / 2058 + 1 + n_bucket; }
 
-
 void run_tile_batch(const BatchArgs &a) {
     Context &c = ctx();
     const uint32_t n_tiles = (uint32_t)ceil_div(a.U, kTile);
 
     // medium tables: cached per distinct prime set
+    constexpr int kWarps = kThreads / 32;
     if (g_med.key != *a.med_primes || !g_med.buf.ptr) {
         MedTables t = build_med(*a.med_primes);
+        if (t.n_tasks > (uint32_t)kMaxTasks) throw Error{SQF2K_ECUDA, "medium task table overflow"};
         g_med.key = *a.med_primes;
         g_med.n_med = t.n_med;
-        g_med.n_items = t.n_items;
-        g_med.buf.reserve((2 * kMaxMed + 2 * kMaxItems) * 4);
-        std::vector<uint32_t> host(2 * kMaxMed + 2 * kMaxItems, 0);
+        g_med.n_tasks = t.n_tasks;
+        const size_t words = 2 * kMaxMed + 64 * kMaxTasks + kWarps + 1;
+        g_med.buf.reserve(words * 4);
+        std::vector<uint32_t> host(words, 0);
         std::copy(t.med.begin(), t.med.end(), host.begin());
-        std::copy(t.items.begin(), t.items.end(), host.begin() + 2 * kMaxMed);
+        std::copy(t.tasks.begin(), t.tasks.end(), host.begin() + 2 * kMaxMed);
+        std::copy(t.beg.begin(), t.beg.end(), host.begin() + 2 * kMaxMed + 64 * kMaxTasks);
         SQF2K_CUDA(cudaMemcpy(g_med.buf.ptr, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
     }
 
@@ -453,23 +577,34 @@ void run_tile_batch(const BatchArgs &a) {
     launch("pattern", pattern_kernel, dim3(ceil_div(kPatWords, 256)), dim3(256), 0, a.base_n,
            a.pattern_present, c.pattern.as<uint32_t>());
 
-    // bucket lists: count, scan, fill (sizes bounded on the host: no sync)
+    // bucket lists (sizes bounded on the host: no sync)
     c.tile_counts.reserve((n_tiles + 1) * 4);
-    c.tile_offsets.reserve((n_tiles + 1) * 4);
     uint32_t *counts = c.tile_counts.as<uint32_t>();
-    uint32_t *offsets = c.tile_offsets.as<uint32_t>();
     SQF2K_CUDA(cudaMemsetAsync(counts, 0, (n_tiles + 1) * 4, c.stream));
     const unsigned bgrid = (unsigned)c.sm_count * 8;
-    c.hits.reserve(bucket_hits_bound(a.U, a.n_primes_bound) * 2 + 64);
-    launch("bucket_count", bucket_kernel<false>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
-           a.base_n, a.U, counts, (const uint32_t *)offsets, (uint16_t *)nullptr);
-    size_t tmp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, (int)n_tiles + 1, c.stream);
-    c.scan_tmp.reserve(std::max<size_t>(tmp_bytes, 64));
-    SQF2K_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.ptr, tmp_bytes, counts, offsets,
-                                             (int)n_tiles + 1, c.stream));
-    launch("bucket_fill", bucket_kernel<true>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
-           a.base_n, a.U, counts, (const uint32_t *)offsets, c.hits.as<uint16_t>());
+    const uint32_t *tile_start = nullptr;
+    if (!a.exact_buckets) {
+        c.hits.reserve((size_t)n_tiles * kBucketCap * 2 + 64);
+        launch("bucket_fill", bucket_kernel<0>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
+               a.base_n, a.U, counts, (const uint32_t *)nullptr, c.hits.as<uint16_t>(),
+               a.overflow);
+    } else {
+        c.tile_offsets.reserve((n_tiles + 1) * 4);
+        uint32_t *offsets = c.tile_offsets.as<uint32_t>();
+        c.hits.reserve(bucket_hits_bound(a.U, a.n_primes_bound) * 2 + 64);
+        launch("bucket_count", bucket_kernel<1>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
+               a.base_n, a.U, counts, (const uint32_t *)offsets, (uint16_t *)nullptr, a.overflow);
+        size_t tmp_bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, (int)n_tiles + 1,
+                                      c.stream);
+        c.scan_tmp.reserve(std::max<size_t>(tmp_bytes, 64));
+        SQF2K_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.ptr, tmp_bytes, counts, offsets,
+                                                 (int)n_tiles + 1, c.stream));
+        launch("bucket_fill", bucket_kernel<2>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
+               a.base_n, a.U, counts, (const uint32_t *)offsets, c.hits.as<uint16_t>(),
+               a.overflow);
+        tile_start = offsets;
+    }
 
     TileParams P;
     std::memset(&P, 0, sizeof P);
@@ -483,11 +618,13 @@ void run_tile_batch(const BatchArgs &a) {
     P.k_eff = a.k_eff;
     P.k_max = a.k_max;
     P.n_med = g_med.n_med;
-    P.n_items = g_med.n_items;
+
     P.pattern = c.pattern.as<uint32_t>();
     P.med = g_med.buf.as<uint32_t>();
-    P.items = g_med.buf.as<uint32_t>() + 2 * kMaxMed;
-    P.tile_start = offsets;
+    P.tasks = reinterpret_cast<const uint2 *>(g_med.buf.as<uint32_t>() + 2 * kMaxMed);
+    P.task_beg = g_med.buf.as<uint32_t>() + 2 * kMaxMed + 64 * kMaxTasks;
+    P.tile_start = tile_start;
+    P.tile_count = counts;
     P.hits = c.hits.as<uint16_t>();
     P.hist = a.hist;
     P.min_n = a.min_n;

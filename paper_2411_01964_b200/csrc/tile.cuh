@@ -40,9 +40,10 @@ constexpr int kHaloMax = 1 << (kDepthMax - 1);
 constexpr int kHaloWordsMax = kHaloMax / 32;
 constexpr uint32_t kPMed = 1024;        // medium primes: 11 <= p < kPMed
 constexpr int kMaxMed = 176;            // pi(1023) - 4 = 168
-constexpr int kMaxItems = 1024;
-constexpr int kItemHits = 8;            // target hits per item per tile
+constexpr int kMaxTasks = 256;          // 32-lane scatter tasks per medium set
+constexpr int kItemHits = 4;            // target hits per lane per tile
 constexpr uint32_t kPatWords = 9 * 25 * 49;  // period of the p = 3, 5, 7 pattern in words
+constexpr int kBucketCap = 64;          // fixed-capacity bucket list per tile (mean ~9)
 constexpr uint32_t kPiBelowPMed = 172;  // pi(1023): table index of the first bucket prime
 constexpr uint32_t kPiSubRoot = 1028;   // pi(8191): last "dense" bucket prime (p^2 < 2^26)
 
@@ -79,11 +80,12 @@ struct TileParams {
     uint32_t k_eff;      // passes inside the tile
     uint32_t k_max;      // run limit: escalate when k_max > k_eff
     uint32_t n_med;
-    uint32_t n_items;
     const uint32_t *pattern;     // kPatWords words of the p = 3, 5, 7 mask, by u-word
     const uint32_t *med;         // per medium prime: q, kTile mod q          (2 x n_med)
-    const uint32_t *items;       // per item: (med << 16 | j), stride          (2 x n_items)
-    const uint32_t *tile_start;  // bucket hit list bounds, n_tiles + 1
+    const uint2 *tasks;          // 32 lane descriptors (m | mult << 8, step) per task
+    const uint32_t *task_beg;    // warp w runs tasks [task_beg[w], task_beg[w+1])
+    const uint32_t *tile_start;  // exact bucket lists: bounds, n_tiles + 1 (or null)
+    const uint32_t *tile_count;  // fixed-capacity lists: hits of tile t at t*kBucketCap
     const uint16_t *hits;        // bucket hits, offsets within the tile
     unsigned long long *hist;    // [65]
     unsigned long long *min_n;   // [65]
@@ -127,6 +129,8 @@ struct BatchArgs {
     unsigned long long *hist, *min_n, *esc, *esc_count, *fail, *fail_count;
     uint64_t esc_cap, fail_cap;
     uint32_t *bits_out;
+    bool exact_buckets;           // count + scan + fill instead of fixed capacity
+    unsigned int *overflow;       // set when a fixed-capacity list overflowed
 };
 void run_tile_batch(const BatchArgs &a);
 

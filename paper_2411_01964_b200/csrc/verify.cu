@@ -131,6 +131,7 @@ struct Acc {
     unsigned long long hist[SQF2K_HIST_LEN];
     unsigned long long min_n[SQF2K_HIST_LEN];
     unsigned long long esc_count, fail_count;
+    unsigned int overflow, pad;
 };
 
 unsigned warp_grid(uint64_t items) {
@@ -220,7 +221,8 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
     const SmallSet small = small_set_upto(limit);
 
     uint64_t esc_cap = 1 << 16, dev_fail_cap = std::max<uint64_t>(fail_cap, 1 << 12);
-    for (int attempt = 0; attempt < 4; ++attempt) {
+    bool exact = (o.flags & SQF2K_EXACT_BUCKETS) != 0;
+    for (int attempt = 0; attempt < 5; ++attempt) {
         c.acc.reserve(sizeof(Acc));
         c.esc.reserve(esc_cap * 8);
         c.fail.reserve(dev_fail_cap * 8);
@@ -244,6 +246,8 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
         a.fail = c.fail.as<unsigned long long>();
         a.fail_count = &acc->fail_count;
         a.fail_cap = dev_fail_cap;
+        a.exact_buckets = exact;
+        a.overflow = &acc->overflow;
         for (uint64_t s0 = 0; s0 < n_slots; s0 += batch) {
             const uint64_t sb = std::min(batch, n_slots - s0);
             const uint64_t A = start + 2 * s0;  // first n of the batch
@@ -280,6 +284,10 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
         Acc &h = *static_cast<Acc *>(c.pinned);
         copy_d2h(&h, acc, sizeof h);
         SQF2K_CUDA(cudaStreamSynchronize(c.stream));
+        if (h.overflow) {  // a bucket list outgrew its fixed capacity: exact lists
+            exact = true;
+            continue;
+        }
         if (h.esc_count > esc_cap) {  // rerun with room for every escalation
             esc_cap = h.esc_count + 1024;
             continue;
@@ -364,7 +372,17 @@ int sieve_bits(uint64_t start, uint64_t end, const int64_t *primes_h, uint64_t n
     a.pattern_present = small.present;
     a.med_primes = &small.med;
     a.bits_out = c.bits_out.as<uint32_t>();
-    run_tile_batch(a);
+    c.acc.reserve(sizeof(Acc));
+    a.overflow = &c.acc.as<Acc>()->overflow;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        SQF2K_CUDA(cudaMemsetAsync(a.overflow, 0, sizeof(unsigned int), c.stream));
+        a.exact_buckets = attempt > 0;
+        run_tile_batch(a);
+        unsigned int &ovf = *static_cast<unsigned int *>(c.pinned);
+        copy_d2h(&ovf, a.overflow, sizeof ovf);
+        SQF2K_CUDA(cudaStreamSynchronize(c.stream));
+        if (!ovf) break;
+    }
     copy_d2h(out, c.bits_out.ptr, nbytes);
     SQF2K_CUDA(cudaStreamSynchronize(c.stream));
     return SQF2K_OK;

@@ -235,11 +235,13 @@ def test_verify_matches_oracle_random_ranges():
         end = start + width
         k_max = rng.choice([1, 2, 3, 5, 9, 13, 16, 17, 20, 30])
         want = O.verify(start, end, width=1 << 30, k_max=k_max)
-        for pipeline, depth, batch in [("fused", 0, 0), ("bitmap", 0, 0), ("fused", 4, 1 << 16),
-                                       ("fused", 16, 3 << 16), ("bitmap", 6, 1 << 17)]:
+        for pipeline, depth, batch, exact in [("fused", 0, 0, False), ("bitmap", 0, 0, False),
+                                              ("fused", 4, 1 << 16, False),
+                                              ("fused", 16, 3 << 16, True),
+                                              ("bitmap", 6, 1 << 17, True)]:
             got = verify_range(start, end, k_max, pipeline=pipeline, tile_depth=depth,
-                               batch_slots=batch)
-            ctx = (start, end, k_max, pipeline, depth, batch)
+                               batch_slots=batch, exact_buckets=exact)
+            ctx = (start, end, k_max, pipeline, depth, batch, exact)
             assert got.histogram == want["histogram"], ctx
             assert got.record_candidates == want["record_candidates"], ctx
             assert got.failures == want["failures"], ctx
@@ -260,7 +262,8 @@ def test_escalation_path_forced():
 def test_batch_and_pipeline_invariance_large():
     end = (1 << 33) + 1
     base = verify_range(1, end, 30)
-    for kw in [dict(batch_slots=1 << 28), dict(pipeline="bitmap"), dict(batch_slots=(1 << 26) + (1 << 16))]:
+    for kw in [dict(batch_slots=1 << 28), dict(pipeline="bitmap"), dict(exact_buckets=True),
+               dict(batch_slots=(1 << 26) + (1 << 16))]:
         got = verify_range(1, end, 30, **kw)
         assert got == base, kw
     # conservation: every odd n in (1, 2^33) counted once
