@@ -147,22 +147,28 @@ def run_ours(args) -> dict | None:
     def step_device():
         return verify_range(lo, hi, K_MAX, pipeline=args.pipeline)
 
-    for _ in range(args.warmup):
+    # clocks are sampled from the start of the warm-up to the end of the timed
+    # steps (nvidia-smi samples every 100 ms; the timed steps alone are short)
+    clocks = ClockSampler(local).__enter__()
+    t_warm = time.perf_counter()
+    done = 0
+    while done < args.warmup or time.perf_counter() - t_warm < args.min_warmup_s:
         step_device()
+        done += 1
     # --- device-timed steps (value): no per-kernel events in the way --------
     times = []
     barrier()
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            part = step_device()
-            e1.record(stream)
-            e1.synchronize()
-            times.append(e0.elapsed_time(e1))
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        part = step_device()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    clocks.__exit__(None, None, None)
     barrier()
     # --- per-kernel breakdown: the same steps with every launch bracketed ---
     _lib.profile(True)
@@ -216,7 +222,9 @@ def run_ours(args) -> dict | None:
     traffic = None
     tj = ROOT / "profiles" / "ncu_traffic.json"
     if tj.exists():
-        traffic = json.loads(tj.read_text()).get(name, {}).get("bytes_per_launch")
+        ent = json.loads(tj.read_text()).get(f"{name}@C2")
+        if ent and ent.get("pipeline") == args.pipeline:
+            traffic = ent["dram_bytes_per_launch"]
     launches_per_step = sum(v[0] for v in kstats.values()) / prof_steps
 
     line = {
@@ -255,10 +263,53 @@ def run_ours(args) -> dict | None:
                 "api": "paper_2411_01964_b200.run_verify(RunConfig(...))",
                 "k_sum": rep.summary.k_sum},
         "clocks": clocks.summary(),
+        "warmup_steps_run": done,
     }
+    if world == 1 and not args.no_large:
+        line["large_window"] = large_window(peak)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(sample_end=args.cpu_sample_end)
     return line
+
+
+def large_window(peak: float, log2_width: int = 37) -> dict:
+    """Sustained per-kernel throughput on a 2^log2_width-integer window ending
+    at 2^50 (the C4/C5 regime: 2M bucketed primes), both pipelines:
+    fused tile kernel (odd n/s and the 0.25 B/n HBM-equivalent) and the
+    two-pass bitmap pipeline's export (HBM write) and scan (HBM read)."""
+    from paper_2411_01964_b200 import _lib
+    from paper_2411_01964_b200.runner import verify_range
+
+    end = (1 << 50) + 1
+    start = end - (1 << log2_width)
+    n = (end - start) // 2
+    out = {"window": [start, end], "odd_n": n}
+    for pipeline in ("fused", "bitmap"):
+        verify_range(start, end, K_MAX, pipeline=pipeline)
+        _lib.profile(True)
+        _lib.profile_reset()
+        reps = 3
+        for _ in range(reps):
+            verify_range(start, end, K_MAX, pipeline=pipeline)
+        st = _lib.profile_read()
+        _lib.profile(False)
+        total = sum(v[1] for v in st.values()) / reps
+        res = {"step_kernel_ms": total, "odd_n_per_s": n / (total / 1e3)}
+        for name, (launches, ms) in st.items():
+            per = ms / reps
+            ent = {"ms_per_step": per, "launches_per_step": launches / reps}
+            if name == "tile_fused":
+                gbs = n * BYTES_PER_ODD_N / (per / 1e3) / 1e9
+                ent.update(odd_n_per_s=n / (per / 1e3), hbm_equiv_gbs=gbs, frac=gbs / peak)
+            if name == "tile_export":
+                gbs = n / 8 / (per / 1e3) / 1e9  # one bit per odd n written
+                ent.update(write_gbs=gbs, frac=gbs / peak)
+            if name == "window_scan":
+                gbs = n / 8 / (per / 1e3) / 1e9  # one bit per odd n read
+                ent.update(read_gbs=gbs, frac=gbs / peak)
+            res[name] = ent
+        out[pipeline] = res
+    return out
 
 
 # -------------------------------------------------------- CPU reference ------
@@ -317,6 +368,10 @@ def main() -> None:
     ap.add_argument("--pipeline", choices=["fused", "bitmap"], default="fused")
     ap.add_argument("--cpu-sample-end", type=int, default=C2_END)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--min-warmup-s", type=float, default=1.5,
+                    help="keep warming up (and sampling clocks) at least this long")
+    ap.add_argument("--no-large", action="store_true",
+                    help="skip the 2^37-wide window near 2^50 per-kernel measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -1,0 +1,51 @@
+"""Condensed, committable summary of an ncu --set full report.
+
+    python tools/ncu_summary.py REPORT.ncu-rep > profiles/NAME.txt
+"""
+import csv
+import subprocess
+import sys
+
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(raw.splitlines()))
+hdr, units = rows[0], rows[1]
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("smsp__inst_executed.sum", "warp instructions executed"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % of peak"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__shared_mem_per_block_dynamic", "dynamic smem/block"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("dram__bytes_read.sum", "DRAM bytes read"),
+    ("dram__bytes_write.sum", "DRAM bytes written"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
+    ("lts__t_bytes.sum", "L2 bytes"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput % of peak"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1/smem throughput % of peak"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared-memory wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared-memory bank conflicts"),
+    ("smsp__inst_executed_op_shared_atom.sum", "shared atomics (warp instr)"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active %"),
+]
+for r in rows[2:]:
+    d = dict(zip(hdr, r))
+    print(f"== {d.get('Kernel Name', '?')[:110]}")
+    print(f"   device {d.get('device__attribute_display_name', '')}  "
+          f"SM clock {d.get('smsp__cycles_elapsed.avg.per_second', '')} {units[hdr.index('smsp__cycles_elapsed.avg.per_second')] if 'smsp__cycles_elapsed.avg.per_second' in hdr else ''}")
+    for k, label in KEYS:
+        if k in d:
+            print(f"   {label:<34} {d[k]:>18} {units[hdr.index(k)]}")
+    stalls = []
+    for k, v in d.items():
+        if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+            try:
+                stalls.append((float(v), k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+            except ValueError:
+                pass
+    stalls.sort(reverse=True)
+    print("   stall cycles per issued instruction: " +
+          ", ".join(f"{n} {v:.2f}" for v, n in stalls[:8]))
