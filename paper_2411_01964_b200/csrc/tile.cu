@@ -40,7 +40,7 @@ __global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__res
 
 // -------------------------------------------------------------------------
 // Bucket pass: every hit u of a bucket prime (p >= kPMed, p^2 <= n_max) in the
-// batch domain [0, U), as a 16-bit offset in the list of tile u >> 16.
+// batch domain [0, U), as a 16-bit offset in the list of tile u >> kTileShift.
 // Work units are (prime, sub-range) pairs of <= 5 hits (see kClasses), one
 // flat index space over all classes so each thread runs one short chain.
 //   MODE 0 (fixed): hit i of tile t goes to hits[t * kBucketCap + i]; counts
@@ -85,18 +85,18 @@ __global__ void __launch_bounds__(256) bucket_kernel(
         const uint64_t r = slot_residue(base_n, q);
         const uint64_t lm = lo % q;
         for (uint64_t u = lo + (r >= lm ? r - lm : r + q - lm); u < hi; u += q) {
-            const uint32_t t = (uint32_t)(u >> 16);
+            const uint32_t t = (uint32_t)(u >> kTileShift);
             if (MODE == 0) {
                 const uint32_t pos = atomicAdd(&counts[t], 1u);
                 if (pos < (uint32_t)kBucketCap)
-                    hits[(uint64_t)t * kBucketCap + pos] = (uint16_t)(u & 0xffff);
+                    hits[(uint64_t)t * kBucketCap + pos] = (uint16_t)(u & (kTile - 1));
                 else
                     atomicOr(overflow, 1u);
             } else if (MODE == 1) {
                 atomicAdd(&counts[t], 1u);
             } else {
                 const uint32_t pos = offsets[t] + atomicSub(&counts[t], 1u) - 1u;
-                hits[pos] = (uint16_t)(u & 0xffff);
+                hits[pos] = (uint16_t)(u & (kTile - 1));
             }
         }
     }
@@ -110,11 +110,17 @@ constexpr int kRingWords = 2 * kTileWords;  // 4096 (power of two)
 struct TileSmem {
     uint8_t bytes[kTile];        // 64 KB, 16-byte aligned
     uint32_t ring[kRingWords];   // 16 KB
+    uint16_t bpos[1024];         // byte_pos() of the slots of one 1024-slot block
     uint32_t med_q[kMaxMed], med_tq[kMaxMed], off[kMaxMed];
     unsigned long long first[kDepthMax + 1];
     uint32_t cnt[kDepthMax + 1];  // counts of k >= 5 (rare)
     uint32_t need;
 };
+
+// byte of slot s (< kTile) through the shared lookup table
+__device__ __forceinline__ uint32_t bpos_of(const uint16_t *bpos, uint32_t s) {
+    return (s & ~1023u) | bpos[s & 1023u];
+}
 
 __device__ __forceinline__ void init_bytes(uint8_t *bytes, uint32_t len) {
     const uint4 one = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
@@ -134,9 +140,10 @@ __device__ __forceinline__ void init_tile_bytes(uint8_t *bytes) {
 // off[m] + mult*q[m], then every `step` slots -- a whole warp sweeping one
 // small prime (steps 32*S*q) or 32 independent items of larger primes.  The
 // host sorts descriptors by trip count and balances tasks over the warps.
-__device__ __forceinline__ void scatter_medium(uint8_t *bytes, const uint32_t *off,
-                                               const uint32_t *med_q, const uint2 *tasks,
-                                               const uint32_t *task_beg, uint32_t len) {
+__device__ __forceinline__ void scatter_medium(uint8_t *bytes, const uint16_t *bpos,
+                                               const uint32_t *off, const uint32_t *med_q,
+                                               const uint2 *tasks, const uint32_t *task_beg,
+                                               uint32_t len) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t k1 = __ldg(&task_beg[warp + 1]);
     for (uint32_t tk = __ldg(&task_beg[warp]); tk < k1; ++tk) {
@@ -146,16 +153,16 @@ __device__ __forceinline__ void scatter_medium(uint8_t *bytes, const uint32_t *o
         uint32_t o = off[m] + (d.x >> 8) * med_q[m];
         const uint32_t step = d.y;
         for (; o + step < len; o += 2 * step) {
-            bytes[byte_pos(o)] = 0;
-            bytes[byte_pos(o + step)] = 0;
+            bytes[bpos_of(bpos, o)] = 0;
+            bytes[bpos_of(bpos, o + step)] = 0;
         }
-        if (o < len) bytes[byte_pos(o)] = 0;
+        if (o < len) bytes[bpos_of(bpos, o)] = 0;
     }
 }
 
 // clear the bucket hits of tile t with offsets in [skip, kTile), shifted by -skip
-__device__ __forceinline__ void scatter_bucket(uint8_t *bytes, const TileParams &P, uint32_t t,
-                                               uint32_t skip) {
+__device__ __forceinline__ void scatter_bucket(uint8_t *bytes, const uint16_t *bpos,
+                                               const TileParams &P, uint32_t t, uint32_t skip) {
     uint32_t b, e;
     if (P.tile_start) {
         b = __ldg(&P.tile_start[t]);
@@ -167,7 +174,7 @@ __device__ __forceinline__ void scatter_bucket(uint8_t *bytes, const TileParams 
     // last threads first: the task balance leaves them no lighter than others
     for (uint32_t i = b + (kThreads - 1 - threadIdx.x); i < e; i += kThreads) {
         const uint32_t o = __ldg(&P.hits[i]);
-        if (o >= skip) bytes[byte_pos(o - skip)] = 0;
+        if (o >= skip) bytes[bpos_of(bpos, o - skip)] = 0;
     }
 }
 
@@ -262,30 +269,49 @@ __device__ __noinline__ void scan_residue(TileSmem &S, uint32_t hb, uint32_t w, 
     }
 }
 
-// One pass of the main scan on one word.
-template <bool TRACK>
+// One pass of the main scan on one word; k = 1 is not counted (hist[1] is
+// derived from the scanned-slot count by conservation, see verify.cu).
+template <bool TRACK, bool COUNT>
 __device__ __forceinline__ void pass(uint32_t &pend, uint32_t sl, uint32_t &cnt, int k,
                                      uint32_t need, uint64_t u0, TileSmem &S) {
     const uint32_t nw = pend & sl;
-    cnt += __popc(nw);
+    if (COUNT) cnt += __popc(nw);
     if (TRACK && nw && ((need >> k) & 1u))
         atomicMin(&S.first[k], (unsigned long long)(u0 + __ffs(nw) - 1));
     pend &= ~sl;
 }
 
-// Exponent passes over the tile's words (ring half starting at hb).  EDGE
-// masks the scan range, TRACK records per-k least slots while this CTA still
-// lacks them, KMAIN is the number of unconditional passes (4, or k_eff).
-// Words left pending after pass 4 (~0.4%) finish in one divergent loop per
-// warp after all of the thread's words.
+// Main scan of one word (cur, its left neighbour prv).  Returns the slots
+// left after KMAIN passes.
+template <bool TRACK, int KMAIN>
+__device__ __forceinline__ uint32_t scan_word(uint32_t pend, uint32_t prv, uint32_t cur,
+                                              uint32_t (&c)[5], uint32_t need, uint64_t u0,
+                                              TileSmem &S) {
+    pass<TRACK, false>(pend, __funnelshift_l(prv, cur, 1), c[1], 1, need, u0, S);
+    if (KMAIN >= 2) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 2), c[2], 2, need, u0, S);
+    if (KMAIN >= 3) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 4), c[3], 3, need, u0, S);
+    if (KMAIN >= 4) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 8), c[4], 4, need, u0, S);
+    return pend;
+}
+
+// Exponent passes over the tile (ring half at hb): thread t owns the four
+// consecutive words 4t..4t+3 (one LDS.128 plus the left neighbour).  EDGE
+// masks the scan range, TRACK records per-k least slots while this CTA
+// still lacks them.  Words left after KMAIN passes (~0.4%) finish in one
+// divergent step per warp.
 template <bool EDGE, bool TRACK, int KMAIN>
 __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint32_t hb,
-                                          uint64_t tb, uint32_t need, uint32_t (&c)[5]) {
-    uint32_t left[kWordsPerThread];
+                                          uint64_t tb, uint32_t need, uint32_t (&c)[5],
+                                          unsigned long long &scanned) {
+    const uint32_t w0 = 4 * threadIdx.x;
+    const uint4 cw = *reinterpret_cast<const uint4 *>(&S.ring[hb + w0]);
+    const uint32_t p0 = S.ring[(hb + w0 - 1) & (kRingWords - 1)];
+    const uint32_t cur[4] = {cw.x, cw.y, cw.z, cw.w};
+    const uint32_t prv[4] = {p0, cw.x, cw.y, cw.z};
+    uint32_t left[4];
 #pragma unroll
-    for (int r = 0; r < kWordsPerThread; ++r) {
-        const uint32_t w = threadIdx.x + r * kThreads;
-        const uint64_t u0 = tb + 32ull * w;
+    for (int i = 0; i < 4; ++i) {
+        const uint64_t u0 = tb + 32ull * (w0 + i);
         uint32_t pend = ~0u;
         if (EDGE) {
             if (u0 + 32 <= P.scan_lo || u0 >= P.U) {
@@ -295,48 +321,30 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
                 if (u0 + 32 > P.U) pend &= (1u << (uint32_t)(P.U - u0)) - 1u;
                 if (P.one_u >= u0 && P.one_u < u0 + 32) pend &= ~(1u << (uint32_t)(P.one_u - u0));
             }
+            scanned += __popc(pend);
         }
-        const uint32_t cur = S.ring[hb + w];
-        const uint32_t prv = S.ring[(hb + w - 1) & (kRingWords - 1)];
-        pass<TRACK>(pend, __funnelshift_l(prv, cur, 1), c[1], 1, need, u0, S);
-        if (KMAIN >= 2) pass<TRACK>(pend, __funnelshift_l(prv, cur, 2), c[2], 2, need, u0, S);
-        if (KMAIN >= 3) pass<TRACK>(pend, __funnelshift_l(prv, cur, 4), c[3], 3, need, u0, S);
-        if (KMAIN >= 4) pass<TRACK>(pend, __funnelshift_l(prv, cur, 8), c[4], 4, need, u0, S);
-        left[r] = pend;
+        left[i] = scan_word<TRACK, KMAIN>(pend, prv[i], cur[i], c, need, u0, S);
     }
+    if (!EDGE) scanned += 128;
     if (__any_sync(0xffffffffu, left[0] | left[1] | left[2] | left[3])) {
 #pragma unroll
-        for (int r = 0; r < kWordsPerThread; ++r) {
-            if (!left[r]) continue;
-            const uint32_t w = threadIdx.x + r * kThreads;
-            const uint64_t u0 = tb + 32ull * w;
+        for (int i = 0; i < 4; ++i) {
+            if (!left[i]) continue;
+            const uint64_t u0 = tb + 32ull * (w0 + i);
             if (KMAIN == 4) {
-                scan_residue(S, hb, w, u0, left[r], need, P.k_eff, P.k_max, P.base_n, P.esc,
-                             P.esc_count, P.esc_cap, P.fail, P.fail_count, P.fail_cap);
+                scan_residue(S, hb, w0 + i, u0, left[i], need, P.k_eff, P.k_max, P.base_n,
+                             P.esc, P.esc_count, P.esc_cap, P.fail, P.fail_count, P.fail_cap);
             } else if (P.k_max > P.k_eff) {  // k_eff = KMAIN < 4: leftovers leave the tile
-                spill_word(left[r], u0, P.base_n, P.esc, P.esc_count, P.esc_cap);
+                spill_word(left[i], u0, P.base_n, P.esc, P.esc_count, P.esc_cap);
             } else {
-                spill_word(left[r], u0, P.base_n, P.fail, P.fail_count, P.fail_cap);
+                spill_word(left[i], u0, P.base_n, P.fail, P.fail_count, P.fail_cap);
             }
         }
     }
 }
 
-template <int KMAIN>
-__device__ __forceinline__ void scan_dispatch(TileSmem &S, const TileParams &P, uint32_t hb,
-                                              uint64_t tb, bool edge, uint32_t need,
-                                              uint32_t (&c)[5]) {
-    const bool track = (need & 0x1eu) != 0;
-    if (edge) {
-        if (track) scan_tile<true, true, KMAIN>(S, P, hb, tb, need, c);
-        else scan_tile<true, false, KMAIN>(S, P, hb, tb, need, c);
-    } else {
-        if (track) scan_tile<false, true, KMAIN>(S, P, hb, tb, need, c);
-        else scan_tile<false, false, KMAIN>(S, P, hb, tb, need, c);
-    }
-}
-
-template <bool FUSED>
+// KMAIN = min(k_eff, 4) unconditional passes; the export form ignores it.
+template <bool FUSED, int KMAIN>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TileParams P) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
@@ -347,6 +355,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     const uint32_t H = FUSED ? P.H : 0u;
     const uint32_t HW = H / 32;
     const bool pre = FUSED && t0 > 0;
+    // tiles [ti0, ti1) need no masks: past the scan start, the n < 1 region
+    // and n = 1, and wholly below the domain end
+    uint64_t lo_edge = FUSED ? P.scan_lo : 0ull;
+    if (P.z > lo_edge) lo_edge = P.z;
+    if (FUSED && P.one_u != ~0ull && P.one_u + 1 > lo_edge) lo_edge = P.one_u + 1;
+    const uint32_t ti0 = (uint32_t)((lo_edge + kTile - 1) / kTile);
+    const uint32_t ti1 = (uint32_t)(P.U / kTile);
 
     // medium primes: q, kTile mod q and the first hit at the chunk base b0
     const uint64_t b0 = pre ? (uint64_t)t0 * kTile - H : (uint64_t)t0 * kTile;
@@ -358,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         S.med_tq[m] = __ldg(&P.med[2 * m + 1]);
         S.off[m] = r >= bm ? r - bm : r + q - bm;
     }
+    for (uint32_t s = threadIdx.x; s < 1024; s += kThreads) S.bpos[s] = (uint16_t)byte_pos(s);
     if (threadIdx.x <= kDepthMax) {
         S.first[threadIdx.x] = ~0ull;
         S.cnt[threadIdx.x] = 0;
@@ -372,8 +388,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     if (FUSED) {
         if (pre) {
             // pre-tile: sieve the H slots below the chunk into the halo words
-            scatter_medium(S.bytes, S.off, S.med_q, P.tasks, P.task_beg, H);
-            scatter_bucket(S.bytes, P, t0 - 1, kTile - H);
+            scatter_medium(S.bytes, S.bpos, S.off, S.med_q, P.tasks, P.task_beg, H);
+            scatter_bucket(S.bytes, S.bpos, P, t0 - 1, kTile - H);
             __syncthreads();
             pack_halo(S.bytes, S.ring, hb0 + kRingWords - HW, HW, b0, pbase, P);
             for (uint32_t m = threadIdx.x; m < P.n_med; m += kThreads) {
@@ -383,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             pbase += HW;
             if (pbase >= kPatWords) pbase -= kPatWords;
             __syncthreads();
-            init_bytes(S.bytes, kTile);
+            init_tile_bytes(S.bytes);
         } else {
             for (uint32_t i = threadIdx.x; i < HW; i += kThreads)
                 S.ring[(hb0 + kRingWords - HW + i) & (kRingWords - 1)] = 0u;
@@ -392,17 +408,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     }
 
     uint32_t c[5] = {0, 0, 0, 0, 0};
-    const uint32_t kmain = P.k_eff < 4 ? P.k_eff : 4;
+    unsigned long long scanned = 0;
     for (uint32_t t = t0; t < t1; ++t) {
         const uint64_t tb = (uint64_t)t * kTile;
         const uint32_t hb = (t & 1u) * kTileWords;
+        const bool edge = t < ti0 || t >= ti1;
 #ifndef SQF2K_EXP_NO_SCATTER
-        scatter_medium(S.bytes, S.off, S.med_q, P.tasks, P.task_beg, kTile);
-        scatter_bucket(S.bytes, P, t, 0);
+        scatter_medium(S.bytes, S.bpos, S.off, S.med_q, P.tasks, P.task_beg, kTile);
+        scatter_bucket(S.bytes, S.bpos, P, t, 0);
 #endif
         __syncthreads();
-        const bool edge_pack = tb < P.z || tb + kTile > P.U;
-        if (edge_pack) pack_words<kTileWords, true, false>(S.bytes, S.ring, hb, tb, pbase, P);
+        if (edge) pack_words<kTileWords, true, false>(S.bytes, S.ring, hb, tb, pbase, P);
         else pack_words<kTileWords, false, false>(S.bytes, S.ring, hb, tb, pbase, P);
         advance_offsets(S.off, S.med_q, S.med_tq, P.n_med);
         pbase += kTileWords;
@@ -411,20 +427,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         if (!FUSED) {
             for (uint32_t w = threadIdx.x; w < kTileWords; w += kThreads)
                 P.bits_out[(uint64_t)t * kTileWords + w] = S.ring[hb + w];
-            init_bytes(S.bytes, kTile);
+            init_tile_bytes(S.bytes);
             __syncthreads();
             continue;
         }
         // ---- exponent passes (search.py:368-381) over the packed tile ----
         const uint32_t need = S.need;
-        const bool edge = tb < P.scan_lo || tb + kTile > P.U ||
-                          (P.one_u >= tb && P.one_u < tb + kTile);
 #ifndef SQF2K_EXP_NO_SCAN
-        switch (kmain) {
-            case 1: scan_dispatch<1>(S, P, hb, tb, edge, need, c); break;
-            case 2: scan_dispatch<2>(S, P, hb, tb, edge, need, c); break;
-            case 3: scan_dispatch<3>(S, P, hb, tb, edge, need, c); break;
-            default: scan_dispatch<4>(S, P, hb, tb, edge, need, c); break;
+        if (need & 0x1eu) {
+            if (edge) scan_tile<true, true, KMAIN>(S, P, hb, tb, need, c, scanned);
+            else scan_tile<false, true, KMAIN>(S, P, hb, tb, need, c, scanned);
+        } else {
+            if (edge) scan_tile<true, false, KMAIN>(S, P, hb, tb, need, c, scanned);
+            else scan_tile<false, false, KMAIN>(S, P, hb, tb, need, c, scanned);
         }
 #endif
         if (t + 1 < t1) init_tile_bytes(S.bytes);  // the next tile's bytes
@@ -445,10 +460,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     if (FUSED) {
         const int lane = threadIdx.x & 31;
 #pragma unroll
-        for (int k = 1; k <= 4; ++k) {
+        for (int k = 2; k <= 4; ++k) {
             const uint32_t s = __reduce_add_sync(0xffffffffu, c[k]);
             if (lane == 0 && s) atomicAdd(&P.hist[k], (unsigned long long)s);
         }
+        unsigned long long sc = scanned;
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, d);
+        if (lane == 0 && sc) atomicAdd(P.scanned, sc);
         __syncthreads();
         if (threadIdx.x >= 5 && threadIdx.x <= kDepthMax && S.cnt[threadIdx.x])
             atomicAdd(&P.hist[threadIdx.x], (unsigned long long)S.cnt[threadIdx.x]);
@@ -551,6 +570,17 @@ size_t tile_smem_bytes() { return sizeof(TileSmem); }
 // of (U/p^2 + 1) <= U / (2 * 1029) + n_bucket_primes.
 uint64_t bucket_hits_bound(uint64_t U, uint64_t n_bucket) { return U / 2058 + 1 + n_bucket; }
 
+template <bool FUSED, int KMAIN>
+void launch_tile(const char *name, unsigned grid, size_t smem, const TileParams &P) {
+    static bool attr = false;
+    if (!attr) {
+        SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<FUSED, KMAIN>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    launch(name, tile_kernel<FUSED, KMAIN>, dim3(grid), dim3(kThreads), smem, P);
+}
+
 void run_tile_batch(const BatchArgs &a) {
     Context &c = ctx();
     const uint32_t n_tiles = (uint32_t)ceil_div(a.U, kTile);
@@ -634,26 +664,20 @@ void run_tile_batch(const BatchArgs &a) {
     P.fail = a.fail;
     P.fail_count = a.fail_count;
     P.fail_cap = a.fail_cap;
+    P.scanned = a.scanned;
     P.bits_out = a.bits_out;
 
     const size_t smem = tile_smem_bytes();
     const unsigned grid = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>(n_tiles, (uint64_t)c.sm_count * kCtasPerSm));
-    static bool attr[2] = {false, false};
     if (a.fused) {
-        if (!attr[1]) {
-            SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<true>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr[1] = true;
-        }
-        launch("tile_fused", tile_kernel<true>, dim3(grid), dim3(kThreads), smem, P);
+        const uint32_t kmain = std::min<uint32_t>(a.k_eff, 4);
+        if (kmain == 1) launch_tile<true, 1>("tile_fused", grid, smem, P);
+        else if (kmain == 2) launch_tile<true, 2>("tile_fused", grid, smem, P);
+        else if (kmain == 3) launch_tile<true, 3>("tile_fused", grid, smem, P);
+        else launch_tile<true, 4>("tile_fused", grid, smem, P);
     } else {
-        if (!attr[0]) {
-            SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<false>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr[0] = true;
-        }
-        launch("tile_export", tile_kernel<false>, dim3(grid), dim3(kThreads), smem, P);
+        launch_tile<false, 1>("tile_export", grid, smem, P);
     }
 }
 

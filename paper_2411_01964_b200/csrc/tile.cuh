@@ -30,11 +30,15 @@
 
 namespace sqf2k {
 
-constexpr int kTile = 1 << 16;          // slots per tile
-constexpr int kTileWords = kTile / 32;  // 2048 packed words
-constexpr int kThreads = 512;           // CTA size of the tile kernels
+#ifndef SQF2K_TILE_SHIFT
+#define SQF2K_TILE_SHIFT 15
+#endif
+constexpr int kTileShift = SQF2K_TILE_SHIFT;
+constexpr int kTile = 1 << kTileShift;  // slots per tile (32768)
+constexpr int kTileWords = kTile / 32;  // 1024 packed words
+constexpr int kThreads = kTileWords / 4;  // CTA size: 4 words per thread in pack and scan
 constexpr int kWordsPerThread = kTileWords / kThreads;  // 4
-constexpr int kCtasPerSm = 2;
+constexpr int kCtasPerSm = (1 << 16) / kTile * 2;  // 4 CTAs of 256 threads per SM
 constexpr int kDepthMax = 16;           // max exponent resolved in-tile
 constexpr int kHaloMax = 1 << (kDepthMax - 1);
 constexpr int kHaloWordsMax = kHaloMax / 32;
@@ -95,6 +99,7 @@ struct TileParams {
     unsigned long long *fail;
     unsigned long long *fail_count;
     uint64_t fail_cap;
+    unsigned long long *scanned; // fused mode: odd n entering the scan (hist[1] by conservation)
     uint32_t *bits_out;          // export mode: packed words of the domain
 };
 
@@ -128,6 +133,7 @@ struct BatchArgs {
     const std::vector<uint32_t> *med_primes;
     unsigned long long *hist, *min_n, *esc, *esc_count, *fail, *fail_count;
     uint64_t esc_cap, fail_cap;
+    unsigned long long *scanned;
     uint32_t *bits_out;
     bool exact_buckets;           // count + scan + fill instead of fixed capacity
     unsigned int *overflow;       // set when a fixed-capacity list overflowed

@@ -131,6 +131,7 @@ struct Acc {
     unsigned long long hist[SQF2K_HIST_LEN];
     unsigned long long min_n[SQF2K_HIST_LEN];
     unsigned long long esc_count, fail_count;
+    unsigned long long scanned;  // fused pipeline: odd n that entered the scan
     unsigned int overflow, pad;
 };
 
@@ -248,6 +249,7 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
         a.fail_cap = dev_fail_cap;
         a.exact_buckets = exact;
         a.overflow = &acc->overflow;
+        a.scanned = &acc->scanned;
         for (uint64_t s0 = 0; s0 < n_slots; s0 += batch) {
             const uint64_t sb = std::min(batch, n_slots - s0);
             const uint64_t A = start + 2 * s0;  // first n of the batch
@@ -305,6 +307,17 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
             out->min_n[k] = h.min_n[k];
         }
         const uint64_t n_fail = h.fail_count;
+        if (o.pipeline == 0) {
+            // the fused kernel does not count k = 1: every scanned n is in
+            // exactly one bucket k >= 1 or a failure (coverage checked)
+            const uint64_t expect = n_slots - (start == 1 ? 1 : 0);
+            if (h.scanned != expect)
+                return fail(SQF2K_ECUDA, "scan coverage %llu != %llu odd n",
+                            (unsigned long long)h.scanned, (unsigned long long)expect);
+            uint64_t rest = n_fail;
+            for (int k = 2; k < SQF2K_HIST_LEN; ++k) rest += out->hist[k];
+            out->hist[1] = h.scanned - rest;
+        }
         if (n_fail > fail_cap) {
             uint64_t none = SQF2K_NONE;
             finish_summary(out, &none, 0);
