@@ -37,6 +37,11 @@ int fail(int code, const char *fmt, ...);
 
 // ---- device buffers -----------------------------------------------------------
 
+// bumped whenever a device buffer is (re)allocated: captured graphs hold raw
+// pointers and are only replayed within one generation
+uint64_t dev_alloc_generation();
+void dev_alloc_bump();  // contents of a shared table changed in place
+
 struct DevBuf {
     void *ptr = nullptr;
     size_t bytes = 0;

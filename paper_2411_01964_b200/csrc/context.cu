@@ -29,8 +29,13 @@ int fail(int code, const char *fmt, ...) {
     return code;
 }
 
+static uint64_t g_alloc_gen = 1;
+uint64_t dev_alloc_generation() { return g_alloc_gen; }
+void dev_alloc_bump() { ++g_alloc_gen; }
+
 void DevBuf::reserve(size_t n) {
     if (n <= bytes) return;
+    ++g_alloc_gen;
     release();
     size_t want = n < 256 ? 256 : n;
     cudaError_t e = cudaMalloc(&ptr, want);

@@ -600,6 +600,7 @@ void run_tile_batch(const BatchArgs &a) {
         std::copy(t.tasks.begin(), t.tasks.end(), host.begin() + 2 * kMaxMed);
         std::copy(t.beg.begin(), t.beg.end(), host.begin() + 2 * kMaxMed + 64 * kMaxTasks);
         SQF2K_CUDA(cudaMemcpy(g_med.buf.ptr, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
+        dev_alloc_bump();  // captured graphs read this table
     }
 
     // p = 3, 5, 7 pattern of this domain

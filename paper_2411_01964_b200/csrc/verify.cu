@@ -7,6 +7,7 @@
 //   n = 1 excluded, unresolved n are failures; hist[k] counts, min_n[k] keeps
 //   the least n with k(n) = k (record candidates are its suffix minima).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -201,6 +202,159 @@ int deliver_failures(unsigned long long *fail_dev, uint64_t n_fail, uint64_t *fa
     return SQF2K_OK;
 }
 
+// Everything one verify call puts on the stream, from the prime table to the
+// accumulator readback into pinned memory; no host synchronisation inside.
+struct VerifyPlan {
+    uint64_t start, end, n_slots, batch, limit, esc_cap, dev_fail_cap;
+    uint32_t k_max, k_eff, H, pipeline;
+    bool exact;
+    SmallSet small;
+};
+
+void enqueue_verify(const VerifyPlan &pl) {
+    Context &c = ctx();
+    generate_primes_async(pl.limit);  // prime table up to isqrt(end - 1) (runner.py:192)
+    c.acc.reserve(sizeof(Acc));
+    c.esc.reserve(pl.esc_cap * 8);
+    c.fail.reserve(pl.dev_fail_cap * 8);
+    Acc *acc = c.acc.as<Acc>();
+    SQF2K_CUDA(cudaMemsetAsync(acc, 0, sizeof(Acc), c.stream));
+    SQF2K_CUDA(cudaMemsetAsync(acc->min_n, 0xff, sizeof acc->min_n, c.stream));
+    BatchArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.k_eff = pl.k_eff;
+    a.k_max = pl.k_max;
+    a.primes = c.primes_u32.as<uint32_t>();
+    a.info = c.prime_info.as<PrimeInfo>();
+    a.n_primes_bound = pi_upper(pl.limit);
+    a.pattern_present = pl.small.present;
+    a.med_primes = &pl.small.med;
+    a.hist = acc->hist;
+    a.min_n = acc->min_n;
+    a.esc = c.esc.as<unsigned long long>();
+    a.esc_count = &acc->esc_count;
+    a.esc_cap = pl.esc_cap;
+    a.fail = c.fail.as<unsigned long long>();
+    a.fail_count = &acc->fail_count;
+    a.fail_cap = pl.dev_fail_cap;
+    a.exact_buckets = pl.exact;
+    a.overflow = &acc->overflow;
+    a.scanned = &acc->scanned;
+    const uint32_t H = pl.H;
+    for (uint64_t s0 = 0; s0 < pl.n_slots; s0 += pl.batch) {
+        const uint64_t sb = std::min(pl.batch, pl.n_slots - s0);
+        const uint64_t A = pl.start + 2 * s0;  // first n of the batch
+        a.base_n = (int64_t)A - 2 * (int64_t)H;
+        a.U = H + sb;
+        a.z = a.base_n < 1 ? (uint64_t)((1 - a.base_n) / 2) : 0;
+        if (pl.pipeline == 1) {
+            // two-pass: export the bitmap of [A - 2H, A + 2 sb) then scan it
+            const uint32_t nt = (uint32_t)ceil_div(a.U, kTile);
+            c.window.reserve((size_t)nt * kTile / 8 + 64);
+            a.fused = false;
+            a.scan_lo = 0;
+            a.one_u = ~0ull;
+            a.H = 0;
+            a.bits_out = c.window.as<uint32_t>();
+            run_tile_batch(a);
+            scan_bitmap_device(c.window.as<uint32_t>(), H / 32, sb, A, pl.k_eff, pl.k_max,
+                               A == 1 ? 0 : ~0ull, acc->hist, acc->min_n, a.esc, a.esc_count,
+                               pl.esc_cap, a.fail, a.fail_count, pl.dev_fail_cap);
+        } else {
+            a.fused = true;
+            a.scan_lo = H;
+            a.one_u = A == 1 ? (uint64_t)H : ~0ull;
+            a.H = H;
+            a.bits_out = nullptr;
+            run_tile_batch(a);
+        }
+    }
+    if (pl.k_max > pl.k_eff)
+        launch("escalate", escalate_kernel, dim3(warp_grid(pl.esc_cap)), dim3(256), 0,
+               (const unsigned long long *)a.esc, (const unsigned long long *)a.esc_count,
+               pl.esc_cap, pl.k_eff + 1, pl.k_max, a.primes, a.info, acc->hist, acc->min_n,
+               a.fail, a.fail_count, pl.dev_fail_cap);
+    copy_d2h(c.pinned, acc, sizeof(Acc));
+}
+
+// Replay cache: the launch sequence of a call is a pure function of its
+// arguments, so it is captured once into a CUDA graph and replayed (every
+// kernel still runs on every call; only the CPU launch cost goes away).
+// Entries die whenever a device buffer is reallocated.
+struct GraphEntry {
+    uint64_t key[8];
+    uint64_t gen;
+    uint64_t h2d, d2h;  // copy accounting of one call
+    cudaGraphExec_t exec;
+};
+std::vector<GraphEntry> g_graphs;
+
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("SQF2K_NO_GRAPHS");
+        return !(e && *e && *e != '0');
+    }();
+    return on && !ctx().profiling;
+}
+
+void plan_key(const VerifyPlan &pl, uint64_t key[8]) {
+    key[0] = pl.start;
+    key[1] = pl.end;
+    key[2] = pl.k_max | ((uint64_t)pl.k_eff << 8) | ((uint64_t)pl.pipeline << 16) |
+             ((uint64_t)pl.exact << 24);
+    key[3] = pl.batch;
+    key[4] = pl.esc_cap;
+    key[5] = pl.dev_fail_cap;
+    key[6] = pl.H;
+    key[7] = 0;
+}
+
+GraphEntry *find_graph(const uint64_t key[8]) {
+    for (auto &g : g_graphs)
+        if (g.gen == dev_alloc_generation() && std::memcmp(g.key, key, sizeof g.key) == 0) return &g;
+    return nullptr;
+}
+
+void capture_graph(const VerifyPlan &pl, const uint64_t key[8]) {
+    Context &c = ctx();
+    const uint64_t gen = dev_alloc_generation(), h2d = c.h2d_bytes, d2h = c.d2h_bytes;
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    bool ok = true;
+    try {
+        enqueue_verify(pl);
+    } catch (const Error &) {
+        ok = false;
+    }
+    if (cudaStreamEndCapture(c.stream, &graph) != cudaSuccess) ok = false;
+    cudaGetLastError();
+    GraphEntry e;
+    std::memcpy(e.key, key, sizeof e.key);
+    e.gen = gen;
+    e.h2d = c.h2d_bytes - h2d;
+    e.d2h = c.d2h_bytes - d2h;
+    c.h2d_bytes = h2d;  // capturing copied nothing
+    c.d2h_bytes = d2h;
+    if (ok && graph && dev_alloc_generation() == gen &&
+        cudaGraphInstantiate(&e.exec, graph, 0) == cudaSuccess) {
+        for (auto &g : g_graphs)
+            if (g.gen != gen) cudaGraphExecDestroy(g.exec);
+        g_graphs.erase(std::remove_if(g_graphs.begin(), g_graphs.end(),
+                                      [gen](const GraphEntry &g) { return g.gen != gen; }),
+                       g_graphs.end());
+        if (g_graphs.size() >= 16) {
+            cudaGraphExecDestroy(g_graphs.front().exec);
+            g_graphs.erase(g_graphs.begin());
+        }
+        g_graphs.push_back(e);
+    }
+    cudaGetLastError();
+    if (graph) cudaGraphDestroy(graph);
+}
+
 // The verify driver: batches of independent sub-ranges, one host sync.
 int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verify_opts_t &o,
                  sqf2k_summary_t *out, uint64_t *failures, uint64_t fail_cap) {
@@ -208,96 +362,49 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
     const uint32_t depth = o.tile_depth ? o.tile_depth : kDepthMax;
     if (depth < 1 || depth > (uint32_t)kDepthMax)
         return fail(SQF2K_EINVAL, "tile_depth must be in 1..%d", kDepthMax);
-    const uint32_t k_eff = std::min(k_max, depth);
-    const uint32_t H = std::max<uint32_t>(1024u, 1u << (k_eff - 1));
-    uint64_t batch = o.batch_slots ? o.batch_slots : kDefaultBatch;
-    batch = std::max<uint64_t>(batch, (uint64_t)kTile);
-    const uint64_t n_slots = (end - start) / 2;
+    VerifyPlan pl;
+    pl.start = start;
+    pl.end = end;
+    pl.k_max = k_max;
+    pl.k_eff = std::min(k_max, depth);
+    pl.H = std::max<uint32_t>(1024u, 1u << (pl.k_eff - 1));
+    pl.batch = std::max<uint64_t>(o.batch_slots ? o.batch_slots : kDefaultBatch, (uint64_t)kTile);
+    pl.n_slots = (end - start) / 2;
+    pl.limit = isqrt_u64(end - 1);
+    pl.pipeline = o.pipeline;
+    pl.small = small_set_upto(pl.limit);
+    pl.esc_cap = 1 << 16;
+    pl.dev_fail_cap = std::max<uint64_t>(fail_cap, 1 << 12);
+    pl.exact = (o.flags & SQF2K_EXACT_BUCKETS) != 0;
+    const uint64_t n_slots = pl.n_slots;
 
-    // prime table up to isqrt(end - 1) (runner.py:192), generated on the GPU
-    const uint64_t limit = isqrt_u64(end - 1);
-    generate_primes_async(limit);
-    const uint32_t *primes = c.primes_u32.as<uint32_t>();
-    const PrimeInfo *info = c.prime_info.as<PrimeInfo>();
-    const SmallSet small = small_set_upto(limit);
-
-    uint64_t esc_cap = 1 << 16, dev_fail_cap = std::max<uint64_t>(fail_cap, 1 << 12);
-    bool exact = (o.flags & SQF2K_EXACT_BUCKETS) != 0;
     for (int attempt = 0; attempt < 5; ++attempt) {
-        c.acc.reserve(sizeof(Acc));
-        c.esc.reserve(esc_cap * 8);
-        c.fail.reserve(dev_fail_cap * 8);
-        Acc *acc = c.acc.as<Acc>();
-        SQF2K_CUDA(cudaMemsetAsync(acc, 0, sizeof(Acc), c.stream));
-        SQF2K_CUDA(cudaMemsetAsync(acc->min_n, 0xff, sizeof acc->min_n, c.stream));
-        BatchArgs a;
-        std::memset(&a, 0, sizeof a);
-        a.k_eff = k_eff;
-        a.k_max = k_max;
-        a.primes = primes;
-        a.info = info;
-        a.n_primes_bound = pi_upper(limit);
-        a.pattern_present = small.present;
-        a.med_primes = &small.med;
-        a.hist = acc->hist;
-        a.min_n = acc->min_n;
-        a.esc = c.esc.as<unsigned long long>();
-        a.esc_count = &acc->esc_count;
-        a.esc_cap = esc_cap;
-        a.fail = c.fail.as<unsigned long long>();
-        a.fail_count = &acc->fail_count;
-        a.fail_cap = dev_fail_cap;
-        a.exact_buckets = exact;
-        a.overflow = &acc->overflow;
-        a.scanned = &acc->scanned;
-        for (uint64_t s0 = 0; s0 < n_slots; s0 += batch) {
-            const uint64_t sb = std::min(batch, n_slots - s0);
-            const uint64_t A = start + 2 * s0;  // first n of the batch
-            a.base_n = (int64_t)A - 2 * (int64_t)H;
-            a.U = H + sb;
-            a.z = a.base_n < 1 ? (uint64_t)((1 - a.base_n) / 2) : 0;
-            if (o.pipeline == 1) {
-                // two-pass: export the bitmap of [A - 2H, A + 2 sb) then scan it
-                const uint32_t nt = (uint32_t)ceil_div(a.U, kTile);
-                c.window.reserve((size_t)nt * kTile / 8 + 64);
-                a.fused = false;
-                a.scan_lo = 0;
-                a.one_u = ~0ull;
-                a.H = 0;
-                a.bits_out = c.window.as<uint32_t>();
-                run_tile_batch(a);
-                scan_bitmap_device(c.window.as<uint32_t>(), H / 32, sb, A, k_eff, k_max,
-                                   A == 1 ? 0 : ~0ull, acc->hist, acc->min_n, a.esc,
-                                   a.esc_count, esc_cap, a.fail, a.fail_count, dev_fail_cap);
-            } else {
-                a.fused = true;
-                a.scan_lo = H;
-                a.one_u = A == 1 ? (uint64_t)H : ~0ull;
-                a.H = H;
-                a.bits_out = nullptr;
-                run_tile_batch(a);
-            }
+        uint64_t key[8];
+        plan_key(pl, key);
+        const bool graphs = graphs_enabled();
+        GraphEntry *g = graphs ? find_graph(key) : nullptr;
+        if (g) {
+            SQF2K_CUDA(cudaGraphLaunch(g->exec, c.stream));
+            c.h2d_bytes += g->h2d;
+            c.d2h_bytes += g->d2h;
+        } else {
+            enqueue_verify(pl);
         }
-        if (k_max > k_eff)
-            launch("escalate", escalate_kernel, dim3(warp_grid(esc_cap)), dim3(256), 0,
-                   (const unsigned long long *)a.esc, (const unsigned long long *)a.esc_count,
-                   esc_cap, k_eff + 1, k_max, primes, info, acc->hist, acc->min_n, a.fail,
-                   a.fail_count, dev_fail_cap);
-        Acc &h = *static_cast<Acc *>(c.pinned);
-        copy_d2h(&h, acc, sizeof h);
         SQF2K_CUDA(cudaStreamSynchronize(c.stream));
+        const Acc h = *static_cast<const Acc *>(c.pinned);
         if (h.overflow) {  // a bucket list outgrew its fixed capacity: exact lists
-            exact = true;
+            pl.exact = true;
             continue;
         }
-        if (h.esc_count > esc_cap) {  // rerun with room for every escalation
-            esc_cap = h.esc_count + 1024;
+        if (h.esc_count > pl.esc_cap) {  // rerun with room for every escalation
+            pl.esc_cap = h.esc_count + 1024;
             continue;
         }
-        if (h.fail_count > dev_fail_cap && h.fail_count <= fail_cap) {
-            dev_fail_cap = h.fail_count + 1024;
+        if (h.fail_count > pl.dev_fail_cap && h.fail_count <= fail_cap) {
+            pl.dev_fail_cap = h.fail_count + 1024;
             continue;
         }
+        if (graphs && !g) capture_graph(pl, key);  // replay the next identical call
         std::memset(out, 0, sizeof *out);
         out->start = start;
         out->end = end;
