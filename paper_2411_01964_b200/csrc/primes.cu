@@ -31,15 +31,17 @@ __device__ void fill_info(PrimeInfo *info, unsigned long long n) {
     for (int j = 0; j <= kClasses; ++j) info->cls[j] = (uint32_t)min(n, (unsigned long long)pi_pow2(j));
 }
 
-// Whole table for limit < 2^17 (one segment) in one CTA: base primes, sieve,
-// ordered compaction and the split.
+// Whole table for limit < 2^17 (one segment) in one CTA: base primes, a byte
+// per odd candidate in shared memory (plain byte stores, no atomics), ordered
+// compaction and the split.
 __global__ void __launch_bounds__(kSieveThreads) prime_small_kernel(uint64_t limit,
                                                                      uint32_t *__restrict__ out,
                                                                      PrimeInfo *__restrict__ info) {
-    __shared__ uint32_t w[kSegWords];
+    extern __shared__ uint8_t flag[];  // flag[i] for the odd number 2i+1
     __shared__ uint32_t base[128];
     __shared__ uint32_t nbase;
     const uint32_t r = (uint32_t)isqrt_u64(limit);  // <= 362
+    const uint32_t n_idx = (uint32_t)((limit + 1) / 2);  // odd numbers <= limit
     if (threadIdx.x < 32) {
         // odd base primes <= r by trial division, ordered by a warp ballot
         uint32_t nb = 0;
@@ -53,43 +55,25 @@ __global__ void __launch_bounds__(kSieveThreads) prime_small_kernel(uint64_t lim
         }
         if (threadIdx.x == 0) nbase = nb;
     }
-    for (int j = threadIdx.x; j < kSegWords; j += blockDim.x) {
-        const uint64_t m0 = 1 + 64ull * j;  // odd numbers 2i+1, i = 32j..32j+31
-        uint32_t word = 0xffffffffu;
-        if (m0 + 62 > limit) {
-            word = 0;
-            for (int b = 0; b < 32; ++b)
-                if (m0 + 2ull * b <= limit) word |= 1u << b;
-        }
-        if (j == 0) word &= ~1u;  // 1 is not prime
-        w[j] = word;
-    }
+    for (uint32_t i = threadIdx.x; i < n_idx; i += blockDim.x) flag[i] = i != 0;  // 1 is not prime
     __syncthreads();
-    const uint32_t n_idx = (uint32_t)((limit + 1) / 2);  // odd numbers <= limit
     for (uint32_t k = 0; k < nbase; ++k) {
         const uint32_t p = base[k];
         for (uint32_t i = (p * p - 1) / 2 + threadIdx.x * p; i < n_idx; i += blockDim.x * p)
-            atomicAnd(&w[i >> 5], ~(1u << (i & 31)));
+            flag[i] = 0;
     }
     __syncthreads();
-    constexpr int kPer = kSegWords / kSieveThreads;
-    uint32_t v[kPer], cnt = 0;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-        v[j] = w[threadIdx.x * kPer + j];
-        cnt += __popc(v[j]);
-    }
+    const uint32_t chunk = (n_idx + blockDim.x - 1) / blockDim.x;
+    const uint32_t lo = min(threadIdx.x * chunk, n_idx), hi = min(lo + chunk, n_idx);
+    uint32_t cnt = 0;
+    for (uint32_t i = lo; i < hi; ++i) cnt += flag[i];
     using Scan = cub::BlockScan<uint32_t, kSieveThreads>;
     __shared__ typename Scan::TempStorage tmp;
     uint32_t off, total;
     Scan(tmp).ExclusiveSum(cnt, off, total);
     uint32_t pos = off + (limit >= 2 ? 1 : 0);
-#pragma unroll
-    for (int j = 0; j < kPer; ++j)
-        for (uint32_t x = v[j]; x; x &= x - 1) {
-            const uint32_t i = (threadIdx.x * kPer + j) * 32 + __ffs(x) - 1;
-            out[pos++] = 2 * i + 1;
-        }
+    for (uint32_t i = lo; i < hi; ++i)
+        if (flag[i]) out[pos++] = 2 * i + 1;
     if (threadIdx.x == 0) {
         if (limit >= 2) out[0] = 2;
         fill_info(info, total + (limit >= 2 ? 1 : 0));
@@ -250,8 +234,14 @@ void generate_primes_async(uint64_t limit) {
     const uint64_t nseg = ceil_div(n_odd, kSegOdds);
     if (nseg == 1) {  // small tables: one CTA does everything
         c.primes_u32.reserve(pi_upper(limit) * 4);
-        launch("primes_small", prime_small_kernel, dim3(1), dim3(kSieveThreads), 0, limit,
-               c.primes_u32.as<uint32_t>(), info);
+        static bool attr = false;
+        if (!attr) {
+            SQF2K_CUDA(cudaFuncSetAttribute(prime_small_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSegOdds));
+            attr = true;
+        }
+        launch("primes_small", prime_small_kernel, dim3(1), dim3(kSieveThreads),
+               (size_t)std::max<uint64_t>(n_odd, 16), limit, c.primes_u32.as<uint32_t>(), info);
         return;
     }
 

@@ -39,7 +39,146 @@ struct ScanParams {
     unsigned long long *fail, *fail_count;
     uint64_t fail_cap;
     uint8_t *kvals;      // exponent-dump mode
+    unsigned long long *scanned;  // fast kernel: odd n entering the scan
 };
+
+// ---------------------------------------------------------------------------
+// Fast summary scan (HBM-bound by design): each thread-iteration covers a
+// group of 4 uint4 = 16 words = 512 slots, read with 4 LDG.128 (+ the word
+// before the group).  Passes k = 1..4 run unconditionally on every word
+// (funnel shifts of the word and its left neighbour); words still pending
+// (~0.4%) continue through k = 5..k_scan with scalar loads.  Blocks own
+// contiguous runs of groups, so each thread sees its slots in increasing
+// order and records the least slot of each k = 1..4 the first time it meets
+// it (register mask, rare-path atomics).  hist[1] is not counted: the host
+// derives it from `scanned` by conservation, as for the fused kernel.
+constexpr int kFastThreads = 256;
+constexpr int kGroupWords = 16;
+
+__device__ __noinline__ void wscan_residue(const ScanParams &P, const uint32_t *__restrict__ w,
+                                           uint64_t word, uint64_t slot0, uint32_t pend,
+                                           uint32_t *s_cnt, unsigned long long *s_first) {
+    const uint32_t cur = w[word], prv = w[word - 1];
+    for (uint32_t k = 5; k <= P.k_scan && pend; ++k) {
+        uint32_t sl;
+        if (k == 5) sl = __funnelshift_l(prv, cur, 16);
+        else if (k == 6) sl = prv;
+        else sl = w[word - (1ull << (k - 6))];
+        const uint32_t nw = pend & sl;
+        if (nw) {
+            atomicAdd(&s_cnt[k], (uint32_t)__popc(nw));
+            atomicMin(&s_first[k], (unsigned long long)(slot0 + __ffs(nw) - 1));
+        }
+        pend &= ~sl;
+    }
+    if (pend) {
+        const bool esc = P.k_max > P.k_scan;
+        for (uint32_t x = pend; x; x &= x - 1) {
+            const uint64_t n = P.first_n + 2 * (slot0 + __ffs(x) - 1);
+            unsigned long long *list = esc ? P.esc : P.fail;
+            unsigned long long *count = esc ? P.esc_count : P.fail_count;
+            const uint64_t cap = esc ? P.esc_cap : P.fail_cap;
+            const unsigned long long j = atomicAdd(count, 1ull);
+            if (j < cap) list[j] = n;
+        }
+    }
+}
+
+template <int KMAIN>
+__global__ void __launch_bounds__(kFastThreads) wscan_kernel(const ScanParams P) {
+    __shared__ unsigned long long s_first[65];
+    __shared__ uint32_t s_cnt[65];
+    for (int k = threadIdx.x; k < 65; k += blockDim.x) {
+        s_first[k] = ~0ull;
+        s_cnt[k] = 0;
+    }
+    __syncthreads();
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(P.w4);
+    const uint64_t word0 = P.c0 * 4;  // word index of slot 0
+    const uint64_t n_groups = (P.n_slots + 32 * kGroupWords - 1) / (32 * kGroupWords);
+    const uint64_t g_lo = n_groups * blockIdx.x / gridDim.x;
+    const uint64_t g_hi = n_groups * (blockIdx.x + 1) / gridDim.x;
+    uint32_t c[5] = {0, 0, 0, 0, 0};
+    unsigned long long scanned = 0;
+    uint32_t tneed = 0x1e;  // k = 1..4 whose least slot this thread has not met yet
+    for (uint64_t g = g_lo + threadIdx.x; g < g_hi; g += blockDim.x) {
+        const uint64_t wg = word0 + g * kGroupWords;
+        uint32_t cur[kGroupWords];
+#pragma unroll
+        for (int v = 0; v < kGroupWords / 4; ++v) {
+            const uint4 x = P.w4[wg / 4 + v];
+            cur[4 * v] = x.x;
+            cur[4 * v + 1] = x.y;
+            cur[4 * v + 2] = x.z;
+            cur[4 * v + 3] = x.w;
+        }
+        uint32_t prv = w[wg - 1];
+        const uint64_t s0 = g * 32 * kGroupWords;  // first slot of the group
+        const bool edge = s0 + 32 * kGroupWords > P.n_slots ||
+                          (P.one_slot >= s0 && P.one_slot < s0 + 32 * kGroupWords);
+        const bool track = __any_sync(__activemask(), tneed);  // lanes may have left the loop
+        uint32_t any = 0;
+        uint32_t left[kGroupWords];
+#pragma unroll
+        for (int i = 0; i < kGroupWords; ++i) {
+            const uint64_t a = s0 + 32 * i;
+            uint32_t pend = ~0u;
+            if (edge) {
+                pend = a >= P.n_slots ? 0u
+                       : (a + 32 <= P.n_slots ? ~0u : ((1u << (uint32_t)(P.n_slots - a)) - 1u));
+                if (P.one_slot >= a && P.one_slot < a + 32) pend &= ~(1u << (uint32_t)(P.one_slot - a));
+                scanned += __popc(pend);
+            }
+            const uint32_t cu = cur[i];
+#pragma unroll
+            for (int k = 1; k <= KMAIN; ++k) {
+                const uint32_t sl = __funnelshift_l(prv, cu, 1u << (k - 1));
+                const uint32_t nw = pend & sl;
+                if (k >= 2) c[k] += __popc(nw);
+                if (track && nw && ((tneed >> k) & 1u)) {
+                    tneed &= ~(1u << k);
+                    atomicMin(&s_first[k], (unsigned long long)(a + __ffs(nw) - 1));
+                }
+                pend &= ~sl;
+            }
+            left[i] = pend;
+            any |= pend;
+            prv = cu;
+        }
+        if (!edge) scanned += 32 * kGroupWords;
+        if (any) {
+#pragma unroll
+            for (int i = 0; i < kGroupWords; ++i)
+                if (left[i]) {
+                    if (KMAIN == 4) {
+                        wscan_residue(P, w, wg + i, s0 + 32 * i, left[i], s_cnt, s_first);
+                    } else {  // k_scan < 4: leftovers are final here
+                        const bool esc = P.k_max > P.k_scan;
+                        for (uint32_t x = left[i]; x; x &= x - 1) {
+                            const uint64_t n = P.first_n + 2 * (s0 + 32 * i + __ffs(x) - 1);
+                            unsigned long long *list = esc ? P.esc : P.fail;
+                            unsigned long long *count = esc ? P.esc_count : P.fail_count;
+                            const unsigned long long j = atomicAdd(count, 1ull);
+                            if (j < (esc ? P.esc_cap : P.fail_cap)) list[j] = n;
+                        }
+                    }
+                }
+        }
+    }
+#pragma unroll
+    for (int k = 2; k <= 4; ++k) {
+        const uint32_t s = __reduce_add_sync(0xffffffffu, c[k]);
+        if ((threadIdx.x & 31) == 0 && s) atomicAdd(&s_cnt[k], s);
+    }
+    for (int d = 16; d >= 1; d >>= 1) scanned += __shfl_xor_sync(0xffffffffu, scanned, d);
+    if ((threadIdx.x & 31) == 0 && scanned) atomicAdd(P.scanned, scanned);
+    __syncthreads();
+    for (int k = threadIdx.x; k < 65; k += blockDim.x) {
+        if (s_cnt[k]) atomicAdd(&P.hist[k], (unsigned long long)s_cnt[k]);
+        if (s_first[k] != ~0ull)
+            atomicMin(&P.min_n[k], (unsigned long long)(P.first_n + 2 * s_first[k]));
+    }
+}
 
 template <bool EXPO>
 __global__ void __launch_bounds__(kScanThreads) window_scan_kernel(const ScanParams P) {
@@ -162,6 +301,7 @@ struct ScanAcc {
     unsigned long long hist[SQF2K_HIST_LEN];
     unsigned long long min_n[SQF2K_HIST_LEN];
     unsigned long long esc_count, fail_count;
+    unsigned long long scanned;
 };
 
 unsigned grid_for(uint64_t n_vec) {
@@ -177,7 +317,7 @@ uint64_t build_window(const uint8_t *prev, uint64_t prev_n, const uint8_t *cur, 
     Context &c = ctx();
     const uint64_t P0 = ceil_div(std::max<uint64_t>(prev_eff, 128), 128) * 128;  // bits
     const uint64_t cur_bytes = ceil_div(cur_n, 64) * 8;
-    const uint64_t total_bits = P0 + ceil_div(cur_n, 128) * 128 + 256;
+    const uint64_t total_bits = P0 + ceil_div(cur_n, 512) * 512 + 1024;  // whole scan groups + pad
     const uint64_t total_bytes = total_bits / 8;
     const uint64_t prev_bytes = prev ? ceil_div(prev_n, 64) * 8 : 0;
     c.window.reserve(total_bytes + prev_bytes + 64);
@@ -238,7 +378,7 @@ void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_sl
                         unsigned long long *hist, unsigned long long *min_n,
                         unsigned long long *esc, unsigned long long *esc_count, uint64_t esc_cap,
                         unsigned long long *fail, unsigned long long *fail_count,
-                        uint64_t fail_cap) {
+                        uint64_t fail_cap, unsigned long long *scanned) {
     ScanParams P;
     std::memset(&P, 0, sizeof P);
     P.w4 = reinterpret_cast<const uint4 *>(words);
@@ -256,8 +396,16 @@ void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_sl
     P.fail = fail;
     P.fail_count = fail_count;
     P.fail_cap = fail_cap;
-    launch("window_scan", window_scan_kernel<false>, dim3(grid_for(ceil_div(n_slots, 128))),
-           dim3(kScanThreads), 0, P);
+    P.scanned = scanned;
+    const uint64_t groups = ceil_div(n_slots, 32 * kGroupWords);
+    const unsigned grid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>(ceil_div(groups, kFastThreads), (uint64_t)ctx().sm_count * 8));
+    switch (std::min<uint32_t>(k_scan, 4)) {
+        case 1: launch("window_scan", wscan_kernel<1>, dim3(grid), dim3(kFastThreads), 0, P); break;
+        case 2: launch("window_scan", wscan_kernel<2>, dim3(grid), dim3(kFastThreads), 0, P); break;
+        case 3: launch("window_scan", wscan_kernel<3>, dim3(grid), dim3(kFastThreads), 0, P); break;
+        default: launch("window_scan", wscan_kernel<4>, dim3(grid), dim3(kFastThreads), 0, P); break;
+    }
 }
 
 }  // namespace sqf2k
@@ -286,7 +434,7 @@ extern "C" int sqf2k_scan_window(const uint8_t *prev_bits, uint64_t prev_start, 
             scan_bitmap_device(c.window.as<uint32_t>(), c0 * 4, cur_n, cur_start, k_max, k_max,
                                cur_start == 1 ? 0 : ~0ull, acc->hist, acc->min_n, nullptr,
                                &acc->esc_count, 0, c.fail.as<unsigned long long>(),
-                               &acc->fail_count, dev_cap);
+                               &acc->fail_count, dev_cap, &acc->scanned);
             ScanAcc h;
             copy_d2h(&h, acc, sizeof h);
             SQF2K_CUDA(cudaStreamSynchronize(c.stream));
@@ -301,6 +449,15 @@ extern "C" int sqf2k_scan_window(const uint8_t *prev_bits, uint64_t prev_start, 
             for (int k = 0; k < SQF2K_HIST_LEN; ++k) {
                 out->hist[k] = h.hist[k];
                 out->min_n[k] = h.min_n[k];
+            }
+            {  // k = 1 is not counted by the kernel: conservation, coverage checked
+                const uint64_t expect = cur_n - (cur_start == 1 ? 1 : 0);
+                if (h.scanned != expect)
+                    return fail(SQF2K_ECUDA, "scan coverage %llu != %llu odd n",
+                                (unsigned long long)h.scanned, (unsigned long long)expect);
+                uint64_t rest = h.fail_count;
+                for (int k = 2; k < SQF2K_HIST_LEN; ++k) rest += h.hist[k];
+                out->hist[1] = h.scanned - rest;
             }
             if (h.fail_count > fail_cap) {
                 out->n_failures = h.fail_count;

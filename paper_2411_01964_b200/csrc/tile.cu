@@ -115,6 +115,11 @@ struct TileSmem {
     unsigned long long first[kDepthMax + 1];
     uint32_t cnt[kDepthMax + 1];  // counts of k >= 5 (rare)
     uint32_t need;
+    // words left after the 4 main passes of the last scanned tile, finished
+    // off the scan's critical path during the next scatter phase
+    uint32_t res_w[kResCap], res_p[kResCap];
+    uint32_t n_res, res_hb;
+    unsigned long long res_tb;
 };
 
 // byte of slot s (< kTile) through the shared lookup table
@@ -303,14 +308,22 @@ template <bool EDGE, bool TRACK, int KMAIN>
 __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint32_t hb,
                                           uint64_t tb, uint32_t need, uint32_t (&c)[5],
                                           unsigned long long &scanned) {
-    const uint32_t w0 = 4 * threadIdx.x;
-    const uint4 cw = *reinterpret_cast<const uint4 *>(&S.ring[hb + w0]);
-    const uint32_t p0 = S.ring[(hb + w0 - 1) & (kRingWords - 1)];
-    const uint32_t cur[4] = {cw.x, cw.y, cw.z, cw.w};
-    const uint32_t prv[4] = {p0, cw.x, cw.y, cw.z};
-    uint32_t left[4];
+    constexpr int W = kWordsPerThread;
+    const uint32_t w0 = W * threadIdx.x;
+    uint32_t cur[W], prv[W];
+    if (W == 4) {
+        const uint4 cw = *reinterpret_cast<const uint4 *>(&S.ring[hb + w0]);
+        cur[0] = cw.x; cur[1 % W] = cw.y; cur[2 % W] = cw.z; cur[3 % W] = cw.w;
+    } else {
+        const uint2 cw = *reinterpret_cast<const uint2 *>(&S.ring[hb + w0]);
+        cur[0] = cw.x; cur[1 % W] = cw.y;
+    }
+    prv[0] = S.ring[(hb + w0 - 1) & (kRingWords - 1)];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 1; i < W; ++i) prv[i] = cur[i - 1];
+    uint32_t left[W], any = 0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
         const uint64_t u0 = tb + 32ull * (w0 + i);
         uint32_t pend = ~0u;
         if (EDGE) {
@@ -324,22 +337,44 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
             scanned += __popc(pend);
         }
         left[i] = scan_word<TRACK, KMAIN>(pend, prv[i], cur[i], c, need, u0, S);
+        any |= left[i];
     }
-    if (!EDGE) scanned += 128;
-    if (__any_sync(0xffffffffu, left[0] | left[1] | left[2] | left[3])) {
+    if (!EDGE) scanned += 32 * W;
+    if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < W; ++i) {
             if (!left[i]) continue;
             const uint64_t u0 = tb + 32ull * (w0 + i);
             if (KMAIN == 4) {
-                scan_residue(S, hb, w0 + i, u0, left[i], need, P.k_eff, P.k_max, P.base_n,
-                             P.esc, P.esc_count, P.esc_cap, P.fail, P.fail_count, P.fail_cap);
+                const uint32_t e = atomicAdd(&S.n_res, 1u);
+                if (e < (uint32_t)kResCap) {  // deferred to the next scatter phase
+                    S.res_w[e] = w0 + i;
+                    S.res_p[e] = left[i];
+                } else {
+                    scan_residue(S, hb, w0 + i, u0, left[i], need, P.k_eff, P.k_max, P.base_n,
+                                 P.esc, P.esc_count, P.esc_cap, P.fail, P.fail_count,
+                                 P.fail_cap);
+                }
             } else if (P.k_max > P.k_eff) {  // k_eff = KMAIN < 4: leftovers leave the tile
                 spill_word(left[i], u0, P.base_n, P.esc, P.esc_count, P.esc_cap);
             } else {
                 spill_word(left[i], u0, P.base_n, P.fail, P.fail_count, P.fail_cap);
             }
         }
+    }
+}
+
+// Finish the deferred words of the last scanned tile (its ring half and the
+// halo below stay intact until the next pack).  Entries are spread over the
+// warps so no warp carries them all.
+__device__ __forceinline__ void drain_residue(TileSmem &S, const TileParams &P) {
+    const uint32_t n = min(S.n_res, (uint32_t)kResCap);
+    if (!n) return;
+    const uint32_t e = (threadIdx.x & 31) * (kThreads / 32) + (threadIdx.x >> 5);
+    if (e < n) {
+        const uint32_t w = S.res_w[e];
+        scan_residue(S, S.res_hb, w, S.res_tb + 32ull * w, S.res_p[e], S.need, P.k_eff, P.k_max,
+                     P.base_n, P.esc, P.esc_count, P.esc_cap, P.fail, P.fail_count, P.fail_cap);
     }
 }
 
@@ -378,7 +413,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         S.first[threadIdx.x] = ~0ull;
         S.cnt[threadIdx.x] = 0;
     }
-    if (threadIdx.x == 0) S.need = ~0u;
+    if (threadIdx.x == 0) {
+        S.need = ~0u;
+        S.n_res = 0;
+    }
     uint32_t pbase = (uint32_t)((b0 / 32) % kPatWords);
     init_bytes(S.bytes, pre ? H : (uint32_t)kTile);
     __syncthreads();
@@ -413,11 +451,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         const uint64_t tb = (uint64_t)t * kTile;
         const uint32_t hb = (t & 1u) * kTileWords;
         const bool edge = t < ti0 || t >= ti1;
+        if (FUSED && KMAIN == 4) drain_residue(S, P);  // the previous tile's leftovers
 #ifndef SQF2K_EXP_NO_SCATTER
         scatter_medium(S.bytes, S.bpos, S.off, S.med_q, P.tasks, P.task_beg, kTile);
         scatter_bucket(S.bytes, S.bpos, P, t, 0);
 #endif
         __syncthreads();
+        if (FUSED && threadIdx.x == 0) {
+            S.n_res = 0;
+            S.res_hb = hb;
+            S.res_tb = tb;
+        }
         if (edge) pack_words<kTileWords, true, false>(S.bytes, S.ring, hb, tb, pbase, P);
         else pack_words<kTileWords, false, false>(S.bytes, S.ring, hb, tb, pbase, P);
         advance_offsets(S.off, S.med_q, S.med_tq, P.n_med);
@@ -444,19 +488,25 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
 #endif
         if (t + 1 < t1) init_tile_bytes(S.bytes);  // the next tile's bytes
         __syncthreads();
-        // per-k least n of this CTA: the first tile where k shows up wins
-        if (threadIdx.x >= 1 && threadIdx.x <= kDepthMax) {
-            const unsigned long long f = S.first[threadIdx.x];
-            if (f != ~0ull) {
-                atomicMin(&P.min_n[threadIdx.x], (unsigned long long)(P.base_n + 2 * (int64_t)f));
-                atomicAnd(&S.need, ~(1u << threadIdx.x));
-                S.first[threadIdx.x] = ~0ull;
-            }
-        }
+        // S.first[k] keeps this CTA's least slot with exponent k (slots grow
+        // with t, so the first tile where k shows up holds it); stop tracking
+        // a k once it is known.  S.first is never reset, so the deferred
+        // residue words (atomicMin during the next scatter) cannot race this.
+        if (threadIdx.x >= 1 && threadIdx.x <= kDepthMax && S.first[threadIdx.x] != ~0ull)
+            atomicAnd(&S.need, ~(1u << threadIdx.x));
         // the next tile's scatter touches only bytes; its pack (which writes
         // the ring half holding this tile's halo source) follows a barrier
     }
 
+    if (FUSED) {  // the last tile's deferred words, then this CTA's minima
+        if (KMAIN == 4) drain_residue(S, P);
+        __syncthreads();
+        if (threadIdx.x >= 1 && threadIdx.x <= kDepthMax) {
+            const unsigned long long f = S.first[threadIdx.x];
+            if (f != ~0ull)
+                atomicMin(&P.min_n[threadIdx.x], (unsigned long long)(P.base_n + 2 * (int64_t)f));
+        }
+    }
     if (FUSED) {
         const int lane = threadIdx.x & 31;
 #pragma unroll

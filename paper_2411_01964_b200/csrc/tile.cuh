@@ -36,9 +36,15 @@ namespace sqf2k {
 constexpr int kTileShift = SQF2K_TILE_SHIFT;
 constexpr int kTile = 1 << kTileShift;  // slots per tile (32768)
 constexpr int kTileWords = kTile / 32;  // 1024 packed words
-constexpr int kThreads = kTileWords / 4;  // CTA size: 4 words per thread in pack and scan
-constexpr int kWordsPerThread = kTileWords / kThreads;  // 4
-constexpr int kCtasPerSm = (1 << 16) / kTile * 2;  // 4 CTAs of 256 threads per SM
+#ifndef SQF2K_WORDS_PER_THREAD
+#define SQF2K_WORDS_PER_THREAD 4
+#endif
+constexpr int kWordsPerThread = SQF2K_WORDS_PER_THREAD;  // words per thread in pack and scan
+constexpr int kThreads = kTileWords / kWordsPerThread;  // CTA size
+#ifndef SQF2K_CTAS_PER_SM
+#define SQF2K_CTAS_PER_SM 4
+#endif
+constexpr int kCtasPerSm = SQF2K_CTAS_PER_SM;
 constexpr int kDepthMax = 16;           // max exponent resolved in-tile
 constexpr int kHaloMax = 1 << (kDepthMax - 1);
 constexpr int kHaloWordsMax = kHaloMax / 32;
@@ -47,6 +53,7 @@ constexpr int kMaxMed = 176;            // pi(1023) - 4 = 168
 constexpr int kMaxTasks = 256;          // 32-lane scatter tasks per medium set
 constexpr int kItemHits = 4;            // target hits per lane per tile
 constexpr uint32_t kPatWords = 9 * 25 * 49;  // period of the p = 3, 5, 7 pattern in words
+constexpr int kResCap = 256;           // deferred residue words per tile
 constexpr int kBucketCap = 64;          // fixed-capacity bucket list per tile (mean ~9)
 constexpr uint32_t kPiBelowPMed = 172;  // pi(1023): table index of the first bucket prime
 constexpr uint32_t kPiSubRoot = 1028;   // pi(8191): last "dense" bucket prime (p^2 < 2^26)

@@ -26,7 +26,7 @@ void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_sl
                         unsigned long long *hist, unsigned long long *min_n,
                         unsigned long long *esc, unsigned long long *esc_count, uint64_t esc_cap,
                         unsigned long long *fail, unsigned long long *fail_count,
-                        uint64_t fail_cap);
+                        uint64_t fail_cap, unsigned long long *scanned);
 
 namespace {
 
@@ -259,7 +259,7 @@ void enqueue_verify(const VerifyPlan &pl) {
             run_tile_batch(a);
             scan_bitmap_device(c.window.as<uint32_t>(), H / 32, sb, A, pl.k_eff, pl.k_max,
                                A == 1 ? 0 : ~0ull, acc->hist, acc->min_n, a.esc, a.esc_count,
-                               pl.esc_cap, a.fail, a.fail_count, pl.dev_fail_cap);
+                               pl.esc_cap, a.fail, a.fail_count, pl.dev_fail_cap, a.scanned);
         } else {
             a.fused = true;
             a.scan_lo = H;
@@ -414,9 +414,9 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
             out->min_n[k] = h.min_n[k];
         }
         const uint64_t n_fail = h.fail_count;
-        if (o.pipeline == 0) {
-            // the fused kernel does not count k = 1: every scanned n is in
-            // exactly one bucket k >= 1 or a failure (coverage checked)
+        {
+            // the kernels do not count k = 1: every scanned n is in exactly
+            // one bucket k >= 1 or a failure (coverage checked)
             const uint64_t expect = n_slots - (start == 1 ? 1 : 0);
             if (h.scanned != expect)
                 return fail(SQF2K_ECUDA, "scan coverage %llu != %llu odd n",
