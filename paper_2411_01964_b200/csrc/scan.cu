@@ -53,19 +53,31 @@ struct ScanParams {
 // it (register mask, rare-path atomics).  hist[1] is not counted: the host
 // derives it from `scanned` by conservation, as for the fused kernel.
 constexpr int kFastThreads = 256;
-constexpr int kGroupWords = 16;
+constexpr int kGroupWords = 8;
 
-__device__ __noinline__ void wscan_residue(const ScanParams &P, const uint32_t *__restrict__ w,
-                                           uint64_t word, uint64_t slot0, uint32_t pend,
-                                           uint32_t *s_cnt, unsigned long long *s_first) {
+// Pending mask of the word starting at slot a (end of range, n = 1).
+__device__ __forceinline__ uint32_t wscan_mask(const ScanParams &P, uint64_t a) {
+    uint32_t pend = a >= P.n_slots ? 0u
+                    : (a + 32 <= P.n_slots ? ~0u : ((1u << (uint32_t)(P.n_slots - a)) - 1u));
+    if (P.one_slot >= a && P.one_slot < a + 32) pend &= ~(1u << (uint32_t)(P.one_slot - a));
+    return pend;
+}
+
+// A word still pending after the main passes (rare): redo passes 1..KMAIN
+// uncounted from the bits in memory, continue up to k_scan, then escalate or
+// fail what is left.
+__device__ void wscan_residue(const ScanParams &P, const uint32_t *__restrict__ w, uint64_t word,
+                              uint64_t slot0, uint32_t kmain, uint32_t *s_cnt,
+                              unsigned long long *s_first) {
     const uint32_t cur = w[word], prv = w[word - 1];
-    for (uint32_t k = 5; k <= P.k_scan && pend; ++k) {
+    uint32_t pend = wscan_mask(P, slot0);
+    for (uint32_t k = 1; k <= P.k_scan && pend; ++k) {
         uint32_t sl;
-        if (k == 5) sl = __funnelshift_l(prv, cur, 16);
+        if (k <= 5) sl = __funnelshift_l(prv, cur, 1u << (k - 1));
         else if (k == 6) sl = prv;
         else sl = w[word - (1ull << (k - 6))];
         const uint32_t nw = pend & sl;
-        if (nw) {
+        if (nw && k > kmain) {
             atomicAdd(&s_cnt[k], (uint32_t)__popc(nw));
             atomicMin(&s_first[k], (unsigned long long)(slot0 + __ffs(nw) - 1));
         }
@@ -84,6 +96,58 @@ __device__ __noinline__ void wscan_residue(const ScanParams &P, const uint32_t *
     }
 }
 
+// One group of kGroupWords words: passes 1..KMAIN on every word, leftovers
+// (~2e-4 of the words after 5 passes) to the residue path.  TRACK records
+// least slots of k = 1..5 the thread has not met yet; EDGE masks the end of
+// the range and n = 1.  The common path (neither) is ~18 ops per 32 slots.
+template <int KMAIN, bool TRACK, bool EDGE>
+__device__ __forceinline__ void wscan_group(const ScanParams &P, const uint32_t *__restrict__ w,
+                                            uint64_t g, uint64_t word0, uint32_t (&c)[6],
+                                            unsigned long long &scanned, uint32_t &tneed,
+                                            uint32_t *s_cnt, unsigned long long *s_first) {
+    const uint64_t wg = word0 + g * kGroupWords;
+    uint32_t cur[kGroupWords];
+#pragma unroll
+    for (int v = 0; v < kGroupWords / 4; ++v) {
+        const uint4 x = P.w4[wg / 4 + v];
+        cur[4 * v] = x.x;
+        cur[4 * v + 1] = x.y;
+        cur[4 * v + 2] = x.z;
+        cur[4 * v + 3] = x.w;
+    }
+    uint32_t prv = w[wg - 1];
+    const uint64_t s0 = g * 32 * kGroupWords;  // first slot of the group
+    uint32_t which = 0;  // words still pending after the main passes
+#pragma unroll
+    for (int i = 0; i < kGroupWords; ++i) {
+        uint32_t pend = ~0u;
+        if (EDGE) {
+            pend = wscan_mask(P, s0 + 32 * i);
+            scanned += __popc(pend);
+        }
+        const uint32_t cu = cur[i];
+#pragma unroll
+        for (int k = 1; k <= KMAIN; ++k) {
+            const uint32_t sl = __funnelshift_l(prv, cu, 1u << (k - 1));
+            const uint32_t nw = pend & sl;
+            if (k >= 2) c[k] += __popc(nw);
+            if (TRACK && nw && ((tneed >> k) & 1u)) {
+                tneed &= ~(1u << k);
+                atomicMin(&s_first[k], (unsigned long long)(s0 + 32 * i + __ffs(nw) - 1));
+            }
+            pend &= ~sl;
+        }
+        which |= (pend != 0u) << i;
+        prv = cu;
+    }
+    if (!EDGE) scanned += 32 * kGroupWords;
+    while (which) {
+        const int i = __ffs(which) - 1;
+        which &= which - 1;
+        wscan_residue(P, w, wg + i, s0 + 32 * i, KMAIN, s_cnt, s_first);
+    }
+}
+
 template <int KMAIN>
 __global__ void __launch_bounds__(kFastThreads) wscan_kernel(const ScanParams P) {
     __shared__ unsigned long long s_first[65];
@@ -98,75 +162,21 @@ __global__ void __launch_bounds__(kFastThreads) wscan_kernel(const ScanParams P)
     const uint64_t n_groups = (P.n_slots + 32 * kGroupWords - 1) / (32 * kGroupWords);
     const uint64_t g_lo = n_groups * blockIdx.x / gridDim.x;
     const uint64_t g_hi = n_groups * (blockIdx.x + 1) / gridDim.x;
-    uint32_t c[5] = {0, 0, 0, 0, 0};
+    uint32_t c[6] = {0, 0, 0, 0, 0, 0};
     unsigned long long scanned = 0;
-    uint32_t tneed = 0x1e;  // k = 1..4 whose least slot this thread has not met yet
+    uint32_t tneed = (2u << KMAIN) - 2u;  // k = 1..KMAIN not met yet by this thread
+    const uint64_t g_edge = P.n_slots / (32 * kGroupWords);  // groups >= this touch the end
+    const uint64_t g_one = P.one_slot == ~0ull ? ~0ull : P.one_slot / (32 * kGroupWords);
     for (uint64_t g = g_lo + threadIdx.x; g < g_hi; g += blockDim.x) {
-        const uint64_t wg = word0 + g * kGroupWords;
-        uint32_t cur[kGroupWords];
-#pragma unroll
-        for (int v = 0; v < kGroupWords / 4; ++v) {
-            const uint4 x = P.w4[wg / 4 + v];
-            cur[4 * v] = x.x;
-            cur[4 * v + 1] = x.y;
-            cur[4 * v + 2] = x.z;
-            cur[4 * v + 3] = x.w;
-        }
-        uint32_t prv = w[wg - 1];
-        const uint64_t s0 = g * 32 * kGroupWords;  // first slot of the group
-        const bool edge = s0 + 32 * kGroupWords > P.n_slots ||
-                          (P.one_slot >= s0 && P.one_slot < s0 + 32 * kGroupWords);
-        const bool track = __any_sync(__activemask(), tneed);  // lanes may have left the loop
-        uint32_t any = 0;
-        uint32_t left[kGroupWords];
-#pragma unroll
-        for (int i = 0; i < kGroupWords; ++i) {
-            const uint64_t a = s0 + 32 * i;
-            uint32_t pend = ~0u;
-            if (edge) {
-                pend = a >= P.n_slots ? 0u
-                       : (a + 32 <= P.n_slots ? ~0u : ((1u << (uint32_t)(P.n_slots - a)) - 1u));
-                if (P.one_slot >= a && P.one_slot < a + 32) pend &= ~(1u << (uint32_t)(P.one_slot - a));
-                scanned += __popc(pend);
-            }
-            const uint32_t cu = cur[i];
-#pragma unroll
-            for (int k = 1; k <= KMAIN; ++k) {
-                const uint32_t sl = __funnelshift_l(prv, cu, 1u << (k - 1));
-                const uint32_t nw = pend & sl;
-                if (k >= 2) c[k] += __popc(nw);
-                if (track && nw && ((tneed >> k) & 1u)) {
-                    tneed &= ~(1u << k);
-                    atomicMin(&s_first[k], (unsigned long long)(a + __ffs(nw) - 1));
-                }
-                pend &= ~sl;
-            }
-            left[i] = pend;
-            any |= pend;
-            prv = cu;
-        }
-        if (!edge) scanned += 32 * kGroupWords;
-        if (any) {
-#pragma unroll
-            for (int i = 0; i < kGroupWords; ++i)
-                if (left[i]) {
-                    if (KMAIN == 4) {
-                        wscan_residue(P, w, wg + i, s0 + 32 * i, left[i], s_cnt, s_first);
-                    } else {  // k_scan < 4: leftovers are final here
-                        const bool esc = P.k_max > P.k_scan;
-                        for (uint32_t x = left[i]; x; x &= x - 1) {
-                            const uint64_t n = P.first_n + 2 * (s0 + 32 * i + __ffs(x) - 1);
-                            unsigned long long *list = esc ? P.esc : P.fail;
-                            unsigned long long *count = esc ? P.esc_count : P.fail_count;
-                            const unsigned long long j = atomicAdd(count, 1ull);
-                            if (j < (esc ? P.esc_cap : P.fail_cap)) list[j] = n;
-                        }
-                    }
-                }
-        }
+        if (g >= g_edge || g == g_one)
+            wscan_group<KMAIN, true, true>(P, w, g, word0, c, scanned, tneed, s_cnt, s_first);
+        else if (tneed)
+            wscan_group<KMAIN, true, false>(P, w, g, word0, c, scanned, tneed, s_cnt, s_first);
+        else
+            wscan_group<KMAIN, false, false>(P, w, g, word0, c, scanned, tneed, s_cnt, s_first);
     }
 #pragma unroll
-    for (int k = 2; k <= 4; ++k) {
+    for (int k = 2; k <= 5; ++k) {
         const uint32_t s = __reduce_add_sync(0xffffffffu, c[k]);
         if ((threadIdx.x & 31) == 0 && s) atomicAdd(&s_cnt[k], s);
     }
@@ -400,11 +410,12 @@ void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_sl
     const uint64_t groups = ceil_div(n_slots, 32 * kGroupWords);
     const unsigned grid = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>(ceil_div(groups, kFastThreads), (uint64_t)ctx().sm_count * 8));
-    switch (std::min<uint32_t>(k_scan, 4)) {
+    switch (std::min<uint32_t>(k_scan, 5)) {
         case 1: launch("window_scan", wscan_kernel<1>, dim3(grid), dim3(kFastThreads), 0, P); break;
         case 2: launch("window_scan", wscan_kernel<2>, dim3(grid), dim3(kFastThreads), 0, P); break;
         case 3: launch("window_scan", wscan_kernel<3>, dim3(grid), dim3(kFastThreads), 0, P); break;
-        default: launch("window_scan", wscan_kernel<4>, dim3(grid), dim3(kFastThreads), 0, P); break;
+        case 4: launch("window_scan", wscan_kernel<4>, dim3(grid), dim3(kFastThreads), 0, P); break;
+        default: launch("window_scan", wscan_kernel<5>, dim3(grid), dim3(kFastThreads), 0, P); break;
     }
 }
 
