@@ -2,6 +2,7 @@
 // the bucketed large-prime hit lists and the tile kernel (fused sieve +
 // min-k scan, or sieve export).  No host synchronisation inside a batch.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -103,14 +104,17 @@ __global__ void __launch_bounds__(256) bucket_kernel(
 }
 
 // -------------------------------------------------------------------------
-// Shared memory of a tile CTA.  The packed words live in a 2-tile ring:
-// tile t occupies half (t & 1), and its halo (the previous tile's last
-// 2^(k_eff-1) slots) is the tail of the other half -- no copy per tile.
-constexpr int kRingWords = 2 * kTileWords;  // 4096 (power of two)
+// Shared memory of a tile CTA.  The tile is sieved directly in packed form:
+// 32-bit words, one bit per odd slot, in a 4-tile ring -- tile t occupies
+// quarter (t & 3) and its halo (the previous tile's last 2^(k_eff-1) slots)
+// is the tail of quarter (t - 1) & 3; starting tile t + 1 (quarter
+// (t + 1) & 3) never touches what tile t's scan or deferred words read.  A word starts as the p = 3, 5, 7 pattern; the
+// medium and bucket primes clear their hits with shared-memory atomics
+// (random scatter: bank-conflict bound at ~9 lanes/cycle/SM on B200, the same
+// rate as byte stores, so no byte array, no pack pass).
+constexpr int kRingWords = 4 * kTileWords;  // power of two
 struct TileSmem {
-    uint8_t bytes[kTile];        // 64 KB, 16-byte aligned
-    uint32_t ring[kRingWords];   // 16 KB
-    uint16_t bpos[1024];         // byte_pos() of the slots of one 1024-slot block
+    uint32_t ring[kRingWords];
     uint32_t med_q[kMaxMed], med_tq[kMaxMed], off[kMaxMed];
     unsigned long long first[kDepthMax + 1];
     uint32_t cnt[kDepthMax + 1];  // counts of k >= 5 (rare)
@@ -122,33 +126,23 @@ struct TileSmem {
     unsigned long long res_tb;
 };
 
-// byte of slot s (< kTile) through the shared lookup table
-__device__ __forceinline__ uint32_t bpos_of(const uint16_t *bpos, uint32_t s) {
-    return (s & ~1023u) | bpos[s & 1023u];
+__device__ __forceinline__ void clear_bit(uint32_t *ring, uint32_t wb, uint32_t o) {
+#ifdef SQF2K_EXP_ATOMIC_AND
+    atomicAnd(&ring[(wb + (o >> 5)) & (kRingWords - 1)], ~(1u << (o & 31)));
+#else
+    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(&ring[(wb + (o >> 5)) & (kRingWords - 1)]);
+    asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(addr), "r"(~(1u << (o & 31))) : "memory");
+#endif
 }
 
-__device__ __forceinline__ void init_bytes(uint8_t *bytes, uint32_t len) {
-    const uint4 one = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
-    for (uint32_t i = threadIdx.x; i < len / 16; i += kThreads)
-        reinterpret_cast<uint4 *>(bytes)[i] = one;
-}
-
-__device__ __forceinline__ void init_tile_bytes(uint8_t *bytes) {
-    const uint4 one = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
-#pragma unroll
-    for (int r = 0; r < kTile / 16 / kThreads; ++r)
-        reinterpret_cast<uint4 *>(bytes)[threadIdx.x + r * kThreads] = one;
-}
-
-// Clear the medium-prime hits in [0, len) of the current base.  Work comes
-// as warp tasks of 32 lane descriptors (m | mult << 8, step): lane clears
-// off[m] + mult*q[m], then every `step` slots -- a whole warp sweeping one
-// small prime (steps 32*S*q) or 32 independent items of larger primes.  The
-// host sorts descriptors by trip count and balances tasks over the warps.
-__device__ __forceinline__ void scatter_medium(uint8_t *bytes, const uint16_t *bpos,
-                                               const uint32_t *off, const uint32_t *med_q,
-                                               const uint2 *tasks, const uint32_t *task_beg,
-                                               uint32_t len) {
+// Clear the medium-prime hits in slots [0, len) of the words starting at
+// ring word wb.  Work comes as warp tasks of 32 lane descriptors (m | mult
+// << 8, step): lane clears off[m] + mult*q[m], then every `step` slots -- a
+// whole warp sweeping one small prime (steps 32*S*q) or 32 independent
+// items of larger primes; the host balances tasks over the warps.
+__device__ __forceinline__ void scatter_medium(uint32_t *ring, uint32_t wb, const uint32_t *off,
+                                               const uint32_t *med_q, const uint2 *tasks,
+                                               const uint32_t *task_beg, uint32_t len) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t k1 = __ldg(&task_beg[warp + 1]);
     for (uint32_t tk = __ldg(&task_beg[warp]); tk < k1; ++tk) {
@@ -158,16 +152,16 @@ __device__ __forceinline__ void scatter_medium(uint8_t *bytes, const uint16_t *b
         uint32_t o = off[m] + (d.x >> 8) * med_q[m];
         const uint32_t step = d.y;
         for (; o + step < len; o += 2 * step) {
-            bytes[bpos_of(bpos, o)] = 0;
-            bytes[bpos_of(bpos, o + step)] = 0;
+            clear_bit(ring, wb, o);
+            clear_bit(ring, wb, o + step);
         }
-        if (o < len) bytes[bpos_of(bpos, o)] = 0;
+        if (o < len) clear_bit(ring, wb, o);
     }
 }
 
 // clear the bucket hits of tile t with offsets in [skip, kTile), shifted by -skip
-__device__ __forceinline__ void scatter_bucket(uint8_t *bytes, const uint16_t *bpos,
-                                               const TileParams &P, uint32_t t, uint32_t skip) {
+__device__ __forceinline__ void scatter_bucket(uint32_t *ring, uint32_t wb, const TileParams &P,
+                                               uint32_t t, uint32_t skip) {
     uint32_t b, e;
     if (P.tile_start) {
         b = __ldg(&P.tile_start[t]);
@@ -179,7 +173,7 @@ __device__ __forceinline__ void scatter_bucket(uint8_t *bytes, const uint16_t *b
     // last threads first: the task balance leaves them no lighter than others
     for (uint32_t i = b + (kThreads - 1 - threadIdx.x); i < e; i += kThreads) {
         const uint32_t o = __ldg(&P.hits[i]);
-        if (o >= skip) bytes[bpos_of(bpos, o - skip)] = 0;
+        if (o >= skip) clear_bit(ring, wb, o - skip);
     }
 }
 
@@ -192,44 +186,36 @@ __device__ __forceinline__ void advance_offsets(uint32_t *off, const uint32_t *m
     }
 }
 
-// Pack WORDS words of bytes (domain slot `base`) into ring[(at + w) & mask].
-// pbase is (base / 32) mod kPatWords.  EDGE applies the n < 1 zero region
-// and the domain end.
-template <int WORDS, bool EDGE, bool WRAP = true>
-__device__ __forceinline__ void pack_words(const uint8_t *bytes, uint32_t *ring, uint32_t at,
-                                           uint64_t base, uint32_t pbase, const TileParams &P) {
+// Start WORDS words (domain slot `base`, ring word `at`) from the p = 3, 5, 7
+// pattern; pbase is (base / 32) mod kPatWords.  EDGE applies the n < 1 zero
+// region and the domain end.
+template <int WORDS, bool EDGE>
+__device__ __forceinline__ void init_words(uint32_t *ring, uint32_t at, uint64_t base,
+                                           uint32_t pbase, const TileParams &P) {
 #pragma unroll
     for (int r = 0; r < (WORDS + kThreads - 1) / kThreads; ++r) {
         const uint32_t w = threadIdx.x + r * kThreads;
         if (WORDS % kThreads != 0 && w >= (uint32_t)WORDS) break;
-        const uint8_t *blk = bytes + ((w >> 5) << 10) + ((w & 31) << 4);
-        const uint4 a = *reinterpret_cast<const uint4 *>(blk);
-        const uint4 b = *reinterpret_cast<const uint4 *>(blk + 512);
-        // bytes are 0/1 and the shifted words never overlap: + is |, and
-        // compiles to a chain of shift-adds
-        uint32_t word = a.x + (a.y << 1) + (a.z << 2) + (a.w << 3) + (b.x << 4) + (b.y << 5) +
-                        (b.z << 6) + (b.w << 7);
-        uint32_t idx = pbase + w;  // pbase < kPatWords, w < kTileWords < kPatWords
+        uint32_t idx = pbase + w;  // pbase < kPatWords, w < kPatWords
         if (idx >= kPatWords) idx -= kPatWords;
-        word &= __ldg(&P.pattern[idx]);
+        uint32_t word = __ldg(&P.pattern[idx]);
         if (EDGE) {
             const uint64_t u0 = base + 32ull * w;
             if (u0 < P.z) word = (u0 + 32 <= P.z) ? 0u : (word & (~0u << (uint32_t)(P.z - u0)));
             if (u0 + 32 > P.U) word = (u0 >= P.U) ? 0u : (word & ((1u << (uint32_t)(P.U - u0)) - 1u));
         }
-        ring[WRAP ? ((at + w) & (kRingWords - 1)) : at + w] = word;
+        ring[(at + w) & (kRingWords - 1)] = word;
     }
 }
 
-// The pre-tile packs H = HW*32 slots (HW in {32, 64, ..., 1024}).
-__device__ __forceinline__ void pack_halo(const uint8_t *bytes, uint32_t *ring, uint32_t at,
-                                          uint32_t HW, uint64_t base, uint32_t pbase,
-                                          const TileParams &P) {
-    if (HW > 512) pack_words<kHaloWordsMax, true>(bytes, ring, at, base, pbase, P);
-    else if (HW > 256) pack_words<512, true>(bytes, ring, at, base, pbase, P);
-    else if (HW > 128) pack_words<256, true>(bytes, ring, at, base, pbase, P);
-    else if (HW > 64) pack_words<128, true>(bytes, ring, at, base, pbase, P);
-    else pack_words<64, true>(bytes, ring, at, base, pbase, P);
+// The pre-tile starts H = HW*32 slots (HW in {32, 64, ..., kTileWords}).
+__device__ __forceinline__ void init_halo(uint32_t *ring, uint32_t at, uint32_t HW, uint64_t base,
+                                          uint32_t pbase, const TileParams &P) {
+    if (HW > kTileWords / 2) init_words<kTileWords, true>(ring, at, base, pbase, P);
+    else if (HW > kTileWords / 4) init_words<kTileWords / 2, true>(ring, at, base, pbase, P);
+    else if (HW > kTileWords / 8) init_words<kTileWords / 4, true>(ring, at, base, pbase, P);
+    else if (HW > kTileWords / 16) init_words<kTileWords / 8, true>(ring, at, base, pbase, P);
+    else init_words<kTileWords / 16, true>(ring, at, base, pbase, P);
 }
 
 __device__ __forceinline__ void append(unsigned long long *list, unsigned long long *count,
@@ -346,8 +332,12 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
             if (!left[i]) continue;
             const uint64_t u0 = tb + 32ull * (w0 + i);
             if (KMAIN == 4) {
+#ifdef SQF2K_EXP_NO_DEFER
+                const uint32_t e = kResCap;
+#else
                 const uint32_t e = atomicAdd(&S.n_res, 1u);
-                if (e < (uint32_t)kResCap) {  // deferred to the next scatter phase
+#endif
+                if (e < (uint32_t)kResCap) {  // deferred to the next start phase
                     S.res_w[e] = w0 + i;
                     S.res_p[e] = left[i];
                 } else {
@@ -364,9 +354,9 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
     }
 }
 
-// Finish the deferred words of the last scanned tile (its ring half and the
-// halo below stay intact until the next pack).  Entries are spread over the
-// warps so no warp carries them all.
+// Finish the deferred words of the last scanned tile (its ring quarter and
+// the halo below stay intact while the next tile starts in another quarter).
+// Entries are spread over the warps so no warp carries them all.
 __device__ __forceinline__ void drain_residue(TileSmem &S, const TileParams &P) {
     const uint32_t n = min(S.n_res, (uint32_t)kResCap);
     if (!n) return;
@@ -379,6 +369,9 @@ __device__ __forceinline__ void drain_residue(TileSmem &S, const TileParams &P) 
 }
 
 // KMAIN = min(k_eff, 4) unconditional passes; the export form ignores it.
+// Per tile: [start words from the pattern] | [scatter the medium and bucket
+// primes' hits as atomic bit clears] | [scan] -- three barriers, two in
+// export mode.
 template <bool FUSED, int KMAIN>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TileParams P) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -408,7 +401,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         S.med_tq[m] = __ldg(&P.med[2 * m + 1]);
         S.off[m] = r >= bm ? r - bm : r + q - bm;
     }
-    for (uint32_t s = threadIdx.x; s < 1024; s += kThreads) S.bpos[s] = (uint16_t)byte_pos(s);
     if (threadIdx.x <= kDepthMax) {
         S.first[threadIdx.x] = ~0ull;
         S.cnt[threadIdx.x] = 0;
@@ -418,62 +410,66 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         S.n_res = 0;
     }
     uint32_t pbase = (uint32_t)((b0 / 32) % kPatWords);
-    init_bytes(S.bytes, pre ? H : (uint32_t)kTile);
-    __syncthreads();
 
-    // ring half of tile t0 and the halo just below it
-    const uint32_t hb0 = (t0 & 1u) * kTileWords;
+    // the halo just below tile t0: the tail of quarter (t0 - 1) & 3
+    const uint32_t halo_at = ((t0 & 3u) * kTileWords + kRingWords - HW) & (kRingWords - 1);
     if (FUSED) {
-        if (pre) {
-            // pre-tile: sieve the H slots below the chunk into the halo words
-            scatter_medium(S.bytes, S.bpos, S.off, S.med_q, P.tasks, P.task_beg, H);
-            scatter_bucket(S.bytes, S.bpos, P, t0 - 1, kTile - H);
+        if (pre) {  // pre-tile: sieve the H slots below the chunk
+            init_halo(S.ring, halo_at, HW, b0, pbase, P);
             __syncthreads();
-            pack_halo(S.bytes, S.ring, hb0 + kRingWords - HW, HW, b0, pbase, P);
+            scatter_medium(S.ring, halo_at, S.off, S.med_q, P.tasks, P.task_beg, H);
+            scatter_bucket(S.ring, halo_at, P, t0 - 1, kTile - H);
+            __syncthreads();
             for (uint32_t m = threadIdx.x; m < P.n_med; m += kThreads) {
                 const uint32_t o = S.off[m] - H % S.med_q[m];
                 S.off[m] = min(o, o + S.med_q[m]);
             }
             pbase += HW;
             if (pbase >= kPatWords) pbase -= kPatWords;
-            __syncthreads();
-            init_tile_bytes(S.bytes);
         } else {
             for (uint32_t i = threadIdx.x; i < HW; i += kThreads)
-                S.ring[(hb0 + kRingWords - HW + i) & (kRingWords - 1)] = 0u;
+                S.ring[(halo_at + i) & (kRingWords - 1)] = 0u;
         }
-        __syncthreads();
     }
+    // S.n_res / S.cnt / S.first must be visible before the first start
+    // phase drains the (empty) residue queue
+    __syncthreads();
 
     uint32_t c[5] = {0, 0, 0, 0, 0};
     unsigned long long scanned = 0;
     for (uint32_t t = t0; t < t1; ++t) {
         const uint64_t tb = (uint64_t)t * kTile;
-        const uint32_t hb = (t & 1u) * kTileWords;
+        const uint32_t hb = (t & 3u) * kTileWords;
         const bool edge = t < ti0 || t >= ti1;
-        if (FUSED && KMAIN == 4) drain_residue(S, P);  // the previous tile's leftovers
-#ifndef SQF2K_EXP_NO_SCATTER
-        scatter_medium(S.bytes, S.bpos, S.off, S.med_q, P.tasks, P.task_beg, kTile);
-        scatter_bucket(S.bytes, S.bpos, P, t, 0);
-#endif
+        // ---- start: pattern words (+ the previous tile's deferred words) ----
+        if (FUSED && KMAIN == 4) drain_residue(S, P);
+        if (edge) init_words<kTileWords, true>(S.ring, hb, tb, pbase, P);
+        else init_words<kTileWords, false>(S.ring, hb, tb, pbase, P);
+        pbase += kTileWords;
+        if (pbase >= kPatWords) pbase -= kPatWords;
+        // S.first[k] keeps this CTA's least slot with exponent k (slots grow
+        // with t, so the first tile where k shows up holds it); stop tracking
+        // a k once it is known.  S.first is never reset, so the deferred
+        // residue words (atomicMin in this phase) cannot race this.
+        if (FUSED && threadIdx.x >= 1 && threadIdx.x <= kDepthMax && S.first[threadIdx.x] != ~0ull)
+            atomicAnd(&S.need, ~(1u << threadIdx.x));
         __syncthreads();
+        // ---- sieve: clear the odd multiples of p^2, p >= 11 ----
         if (FUSED && threadIdx.x == 0) {
             S.n_res = 0;
             S.res_hb = hb;
             S.res_tb = tb;
         }
-        if (edge) pack_words<kTileWords, true, false>(S.bytes, S.ring, hb, tb, pbase, P);
-        else pack_words<kTileWords, false, false>(S.bytes, S.ring, hb, tb, pbase, P);
-        advance_offsets(S.off, S.med_q, S.med_tq, P.n_med);
-        pbase += kTileWords;
-        if (pbase >= kPatWords) pbase -= kPatWords;
+#ifndef SQF2K_EXP_NO_SCATTER
+        scatter_medium(S.ring, hb, S.off, S.med_q, P.tasks, P.task_beg, kTile);
+        scatter_bucket(S.ring, hb, P, t, 0);
+#endif
         __syncthreads();
+        advance_offsets(S.off, S.med_q, S.med_tq, P.n_med);
         if (!FUSED) {
             for (uint32_t w = threadIdx.x; w < kTileWords; w += kThreads)
                 P.bits_out[(uint64_t)t * kTileWords + w] = S.ring[hb + w];
-            init_tile_bytes(S.bytes);
-            __syncthreads();
-            continue;
+            continue;  // the next start writes another quarter; its barrier orders the offsets
         }
         // ---- exponent passes (search.py:368-381) over the packed tile ----
         const uint32_t need = S.need;
@@ -486,16 +482,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             else scan_tile<false, false, KMAIN>(S, P, hb, tb, need, c, scanned);
         }
 #endif
-        if (t + 1 < t1) init_tile_bytes(S.bytes);  // the next tile's bytes
         __syncthreads();
-        // S.first[k] keeps this CTA's least slot with exponent k (slots grow
-        // with t, so the first tile where k shows up holds it); stop tracking
-        // a k once it is known.  S.first is never reset, so the deferred
-        // residue words (atomicMin during the next scatter) cannot race this.
-        if (threadIdx.x >= 1 && threadIdx.x <= kDepthMax && S.first[threadIdx.x] != ~0ull)
-            atomicAnd(&S.need, ~(1u << threadIdx.x));
-        // the next tile's scatter touches only bytes; its pack (which writes
-        // the ring half holding this tile's halo source) follows a barrier
     }
 
     if (FUSED) {  // the last tile's deferred words, then this CTA's minima
@@ -506,8 +493,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             if (f != ~0ull)
                 atomicMin(&P.min_n[threadIdx.x], (unsigned long long)(P.base_n + 2 * (int64_t)f));
         }
-    }
-    if (FUSED) {
         const int lane = threadIdx.x & 31;
 #pragma unroll
         for (int k = 2; k <= 4; ++k) {
@@ -518,7 +503,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
 #pragma unroll
         for (int d = 16; d >= 1; d >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, d);
         if (lane == 0 && sc) atomicAdd(P.scanned, sc);
-        __syncthreads();
         if (threadIdx.x >= 5 && threadIdx.x <= kDepthMax && S.cnt[threadIdx.x])
             atomicAdd(&P.hist[threadIdx.x], (unsigned long long)S.cnt[threadIdx.x]);
     }
@@ -719,8 +703,9 @@ void run_tile_batch(const BatchArgs &a) {
     P.bits_out = a.bits_out;
 
     const size_t smem = tile_smem_bytes();
-    const unsigned grid = (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>(n_tiles, (uint64_t)c.sm_count * kCtasPerSm));
+    uint64_t grid_cap = (uint64_t)c.sm_count * kCtasPerSm;
+    if (const char *g = std::getenv("SQF2K_DEBUG_GRID")) grid_cap = std::max(1, atoi(g));
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(n_tiles, grid_cap));
     if (a.fused) {
         const uint32_t kmain = std::min<uint32_t>(a.k_eff, 4);
         if (kmain == 1) launch_tile<true, 1>("tile_fused", grid, smem, P);

@@ -331,3 +331,19 @@ def test_run_verify_errors():
         run_verify(RunConfig(start=4, end=100))
     with pytest.raises(ConfigError):
         run_verify(RunConfig(start=1, end=(1 << 62) + 2))
+
+
+@pytest.mark.parametrize("depth", [0, 10, 12])
+def test_single_cta_long_runs(monkeypatch, depth):
+    # one CTA walks many tiles, so the 4-quarter smem ring wraps repeatedly
+    # and the first start phase of the t0 = 0 chunk drains an empty queue
+    # (regression: a missing barrier let it drain stale shared memory)
+    monkeypatch.setenv("SQF2K_DEBUG_GRID", "1")
+    for lo, tiles in [(1, 13), ((1 << 33) + 1, 11), ((1 << 46) + 12345, 9)]:
+        hi = lo + 2 * tiles * 32768 + 2 * 777
+        want = O.verify(lo, hi, width=1 << 30, k_max=30)
+        for _ in range(2):
+            got = verify_range(lo, hi, 30, tile_depth=depth)
+            assert got.histogram == want["histogram"], (lo, depth)
+            assert got.k_sum == want["k_sum"]
+            assert got.record_candidates == want["record_candidates"]
