@@ -17,7 +17,9 @@ namespace {
 
 // -------------------------------------------------------------------------
 // p = 3, 5, 7: word g of the domain (slots 32g..32g+31) with every slot u
-// such that 9, 25 or 49 divides n(u) cleared.  Period 11025 words.
+// such that 9, 25 or 49 divides n(u) cleared.  Period 11025 words; the
+// first kTileWords words are repeated after the period so that a tile's
+// words [pbase, pbase + kTileWords) never wrap.
 // First hit at or after 32g: y = (r - 32g) mod q; the word's hits are the
 // bits y, y+q, ... < 32, i.e. (bits 0, q, 2q, ...) << y.
 __global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__restrict__ table) {
@@ -26,7 +28,7 @@ __global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__res
     uint32_t r[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) r[i] = (uint32_t)slot_residue(base_n, q[i]);
-    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < kPatWords;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < kPatWords + kTileWords;
          g += gridDim.x * blockDim.x) {
         uint32_t clr = 0;
 #pragma unroll
@@ -108,60 +110,87 @@ __global__ void __launch_bounds__(256) bucket_kernel(
 // 32-bit words, one bit per odd slot, in a 4-tile ring -- tile t occupies
 // quarter (t & 3) and its halo (the previous tile's last 2^(k_eff-1) slots)
 // is the tail of quarter (t - 1) & 3; starting tile t + 1 (quarter
-// (t + 1) & 3) never touches what tile t's scan or deferred words read.  A word starts as the p = 3, 5, 7 pattern; the
-// medium and bucket primes clear their hits with shared-memory atomics
-// (random scatter: bank-conflict bound at ~9 lanes/cycle/SM on B200, the same
-// rate as byte stores, so no byte array, no pack pass).
+// (t + 1) & 3) never touches what tile t's scan or deferred words read.  A
+// word starts as the p = 3, 5, 7 pattern; the medium and bucket primes clear
+// their hits with shared-memory atomics (random scatter: bank-conflict bound
+// at ~9 lanes/cycle/SM on B200, the same rate as byte stores, so no byte
+// array and no pack pass).
 constexpr int kRingWords = 4 * kTileWords;  // power of two
 struct TileSmem {
     uint32_t ring[kRingWords];
-    uint32_t med_q[kMaxMed], med_tq[kMaxMed], off[kMaxMed];
     unsigned long long first[kDepthMax + 1];
-    uint32_t cnt[kDepthMax + 1];  // counts of k >= 5 (rare)
+    uint32_t cnt[kDepthMax + 1];  // counts of k >= 6 (rare)
     uint32_t need;
-    // words left after the 4 main passes of the last scanned tile, finished
-    // off the scan's critical path during the next scatter phase
+    // words left after the main passes of the last scanned tile, finished
+    // during the next start phase
     uint32_t res_w[kResCap], res_p[kResCap];
     uint32_t n_res, res_hb;
     unsigned long long res_tb;
 };
 
-__device__ __forceinline__ void clear_bit(uint32_t *ring, uint32_t wb, uint32_t o) {
+// Clear slot o of the words starting at shared address wbase (byte address
+// of a run of words that does not wrap): one shift, one LEA, one funnel
+// shift for ~(1 << (o & 31)), one RED.
+__device__ __forceinline__ void clear_bit(uint32_t wbase, uint32_t o) {
+    const uint32_t addr = wbase + ((o >> 5) << 2);
+    const uint32_t m = __funnelshift_l(0xffffffffu, 0xfffffffeu, o);
 #ifdef SQF2K_EXP_ATOMIC_AND
-    atomicAnd(&ring[(wb + (o >> 5)) & (kRingWords - 1)], ~(1u << (o & 31)));
+    atomicAnd(reinterpret_cast<uint32_t *>(__cvta_shared_to_generic(addr)), m);
 #else
-    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(&ring[(wb + (o >> 5)) & (kRingWords - 1)]);
-    asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(addr), "r"(~(1u << (o & 31))) : "memory");
+    asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(addr), "r"(m) : "memory");
 #endif
 }
 
-// Clear the medium-prime hits in slots [0, len) of the words starting at
-// ring word wb.  Work comes as warp tasks of 32 lane descriptors (m | mult
-// << 8, step): lane clears off[m] + mult*q[m], then every `step` slots -- a
-// whole warp sweeping one small prime (steps 32*S*q) or 32 independent
-// items of larger primes; the host balances tasks over the warps.
-__device__ __forceinline__ void scatter_medium(uint32_t *ring, uint32_t wb, const uint32_t *off,
-                                               const uint32_t *med_q, const uint2 *tasks,
-                                               const uint32_t *task_beg, uint32_t len) {
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t k1 = __ldg(&task_beg[warp + 1]);
-    for (uint32_t tk = __ldg(&task_beg[warp]); tk < k1; ++tk) {
-        const uint2 d = __ldg(&tasks[tk * 32 + lane]);
-        if (!d.y) continue;
-        const uint32_t m = d.x & 0xffu;
-        uint32_t o = off[m] + (d.x >> 8) * med_q[m];
-        const uint32_t step = d.y;
-        for (; o + step < len; o += 2 * step) {
-            clear_bit(ring, wb, o);
-            clear_bit(ring, wb, o + step);
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// Medium primes 11 <= p < kPMed.  Each lane owns kTaskSlots descriptors
+// (host-balanced, see build_med): a start hit and a step (a multiple of
+// q = p^2).  o[j] is the lane's next hit relative to the current run of
+// slots; after clearing the hits in [0, len) it is rebased by -len, which
+// is exactly the next run's offset -- the offsets never leave registers.
+struct MedLane {
+    uint32_t o[kTaskSlots], step[kTaskSlots];
+};
+
+__device__ __forceinline__ void scatter_medium(MedLane &L, uint32_t wbase, uint32_t len) {
+#pragma unroll
+    for (int j = 0; j < kTaskSlots; ++j) {
+        const uint32_t st = L.step[j];
+        uint32_t o = L.o[j];
+        for (; o + st < len; o += 2 * st) {
+            clear_bit(wbase, o);
+            clear_bit(wbase, o + st);
         }
-        if (o < len) clear_bit(ring, wb, o);
+        if (o < len) {
+            clear_bit(wbase, o);
+            o += st;
+        }
+        L.o[j] = st ? o - len : o;  // idle slots (step 0) keep o = ~0
+    }
+}
+
+// Load this lane's descriptors and place their first hits at or after slot b0.
+__device__ __forceinline__ void init_medium(MedLane &L, const TileParams &P, uint64_t b0) {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < kTaskSlots; ++j) {
+        const uint2 d = __ldg(&P.tasks[(warp * kTaskSlots + j) * 32 + lane]);
+        L.step[j] = d.y;
+        L.o[j] = ~0u;
+        if (d.y) {
+            const uint32_t q = __ldg(&P.med[d.x & 0xffu]);
+            const uint32_t r = (uint32_t)slot_residue(P.base_n, q);
+            const uint32_t bm = (uint32_t)(b0 % q);
+            L.o[j] = (r >= bm ? r - bm : r + q - bm) + (d.x >> 8) * q;
+        }
     }
 }
 
 // clear the bucket hits of tile t with offsets in [skip, kTile), shifted by -skip
-__device__ __forceinline__ void scatter_bucket(uint32_t *ring, uint32_t wb, const TileParams &P,
-                                               uint32_t t, uint32_t skip) {
+__device__ __forceinline__ void scatter_bucket(uint32_t wbase, const TileParams &P, uint32_t t,
+                                               uint32_t skip) {
     uint32_t b, e;
     if (P.tile_start) {
         b = __ldg(&P.tile_start[t]);
@@ -173,49 +202,44 @@ __device__ __forceinline__ void scatter_bucket(uint32_t *ring, uint32_t wb, cons
     // last threads first: the task balance leaves them no lighter than others
     for (uint32_t i = b + (kThreads - 1 - threadIdx.x); i < e; i += kThreads) {
         const uint32_t o = __ldg(&P.hits[i]);
-        if (o >= skip) clear_bit(ring, wb, o - skip);
+        if (o >= skip) clear_bit(wbase, o - skip);
     }
 }
 
-// move the medium offsets forward by `step[m]` (= len mod q) slots
-__device__ __forceinline__ void advance_offsets(uint32_t *off, const uint32_t *med_q,
-                                                const uint32_t *step, uint32_t n_med) {
-    for (uint32_t m = threadIdx.x; m < n_med; m += kThreads) {
-        const uint32_t o = off[m] - step[m];  // wraps when negative
-        off[m] = min(o, o + med_q[m]);
-    }
-}
-
-// Start WORDS words (domain slot `base`, ring word `at`) from the p = 3, 5, 7
-// pattern; pbase is (base / 32) mod kPatWords.  EDGE applies the n < 1 zero
-// region and the domain end.
+// Start WORDS words (domain slot `base`, ring word `at`, 16-byte aligned and
+// not wrapping) from the p = 3, 5, 7 pattern; pbase is (base / 32) mod
+// kPatWords.  Thread i writes words 4i..4i+3 with one STS.128.  EDGE
+// applies the n < 1 zero region and the domain end.
 template <int WORDS, bool EDGE>
 __device__ __forceinline__ void init_words(uint32_t *ring, uint32_t at, uint64_t base,
                                            uint32_t pbase, const TileParams &P) {
+    static_assert(WORDS % 4 == 0 && WORDS <= 4 * kThreads, "one uint4 per thread");
+    const uint32_t w = 4 * threadIdx.x;
+    if (WORDS < 4 * kThreads && w >= (uint32_t)WORDS) return;
+    const uint32_t *src = P.pattern + pbase + w;  // padded table: no wrap
+    uint32_t v[4];
 #pragma unroll
-    for (int r = 0; r < (WORDS + kThreads - 1) / kThreads; ++r) {
-        const uint32_t w = threadIdx.x + r * kThreads;
-        if (WORDS % kThreads != 0 && w >= (uint32_t)WORDS) break;
-        uint32_t idx = pbase + w;  // pbase < kPatWords, w < kPatWords
-        if (idx >= kPatWords) idx -= kPatWords;
-        uint32_t word = __ldg(&P.pattern[idx]);
-        if (EDGE) {
-            const uint64_t u0 = base + 32ull * w;
-            if (u0 < P.z) word = (u0 + 32 <= P.z) ? 0u : (word & (~0u << (uint32_t)(P.z - u0)));
-            if (u0 + 32 > P.U) word = (u0 >= P.U) ? 0u : (word & ((1u << (uint32_t)(P.U - u0)) - 1u));
+    for (int i = 0; i < 4; ++i) v[i] = __ldg(src + i);
+    if (EDGE) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint64_t u0 = base + 32ull * (w + i);
+            if (u0 < P.z) v[i] = (u0 + 32 <= P.z) ? 0u : (v[i] & (~0u << (uint32_t)(P.z - u0)));
+            if (u0 + 32 > P.U) v[i] = (u0 >= P.U) ? 0u : (v[i] & ((1u << (uint32_t)(P.U - u0)) - 1u));
         }
-        ring[(at + w) & (kRingWords - 1)] = word;
     }
+    *reinterpret_cast<uint4 *>(&ring[at + w]) = make_uint4(v[0], v[1], v[2], v[3]);
 }
 
-// The pre-tile starts H = HW*32 slots (HW in {32, 64, ..., kTileWords}).
+// The pre-tile starts the H = HW*32 halo slots (HW in {32, 64, ..., kTileWords}).
 __device__ __forceinline__ void init_halo(uint32_t *ring, uint32_t at, uint32_t HW, uint64_t base,
                                           uint32_t pbase, const TileParams &P) {
-    if (HW > kTileWords / 2) init_words<kTileWords, true>(ring, at, base, pbase, P);
-    else if (HW > kTileWords / 4) init_words<kTileWords / 2, true>(ring, at, base, pbase, P);
-    else if (HW > kTileWords / 8) init_words<kTileWords / 4, true>(ring, at, base, pbase, P);
-    else if (HW > kTileWords / 16) init_words<kTileWords / 8, true>(ring, at, base, pbase, P);
-    else init_words<kTileWords / 16, true>(ring, at, base, pbase, P);
+    if (HW == kTileWords) init_words<kTileWords, true>(ring, at, base, pbase, P);
+    else if (HW == kTileWords / 2) init_words<kTileWords / 2, true>(ring, at, base, pbase, P);
+    else if (HW == kTileWords / 4) init_words<kTileWords / 4, true>(ring, at, base, pbase, P);
+    else if (HW == kTileWords / 8) init_words<kTileWords / 8, true>(ring, at, base, pbase, P);
+    else if (HW == kTileWords / 16) init_words<kTileWords / 16, true>(ring, at, base, pbase, P);
+    else init_words<kTileWords / 32, true>(ring, at, base, pbase, P);
 }
 
 __device__ __forceinline__ void append(unsigned long long *list, unsigned long long *count,
@@ -233,20 +257,15 @@ __device__ __noinline__ void spill_word(uint32_t pend, uint64_t u0, int64_t base
         append(list, count, cap, (uint64_t)(base_n + 2 * (int64_t)(u0 + __ffs(x) - 1)));
 }
 
-// Passes k = 5..k_eff for one word (divergent, rare: ~0.4% of words).
+// Passes k = 6..k_eff for one word (divergent, rare: ~0.02% of words).
 __device__ __noinline__ void scan_residue(TileSmem &S, uint32_t hb, uint32_t w, uint64_t u0,
                                           uint32_t pend, uint32_t need, uint32_t k_eff,
                                           uint32_t k_max, int64_t base_n, unsigned long long *esc,
                                           unsigned long long *esc_count, uint64_t esc_cap,
                                           unsigned long long *fail,
                                           unsigned long long *fail_count, uint64_t fail_cap) {
-    const uint32_t cur = S.ring[(hb + w) & (kRingWords - 1)];
-    const uint32_t prv = S.ring[(hb + w - 1) & (kRingWords - 1)];
-    for (uint32_t k = 5; k <= k_eff && pend; ++k) {
-        uint32_t sl;
-        if (k == 5) sl = __funnelshift_l(prv, cur, 16);
-        else if (k == 6) sl = prv;
-        else sl = S.ring[(hb + w - (1u << (k - 6))) & (kRingWords - 1)];
+    for (uint32_t k = 6; k <= k_eff && pend; ++k) {
+        const uint32_t sl = S.ring[(hb + w - (1u << (k - 6))) & (kRingWords - 1)];
         const uint32_t nw = pend & sl;
         if (nw) {
             atomicAdd(&S.cnt[k], (uint32_t)__popc(nw));
@@ -272,27 +291,29 @@ __device__ __forceinline__ void pass(uint32_t &pend, uint32_t sl, uint32_t &cnt,
     pend &= ~sl;
 }
 
-// Main scan of one word (cur, its left neighbour prv).  Returns the slots
-// left after KMAIN passes.
+// Main scan of one word (cur, its left neighbour prv): n - 2^k for k <= 5 is
+// 2^(k-1) slots back, inside (cur, prv).  Returns the slots left after KMAIN
+// passes.
 template <bool TRACK, int KMAIN>
 __device__ __forceinline__ uint32_t scan_word(uint32_t pend, uint32_t prv, uint32_t cur,
-                                              uint32_t (&c)[5], uint32_t need, uint64_t u0,
+                                              uint32_t (&c)[6], uint32_t need, uint64_t u0,
                                               TileSmem &S) {
     pass<TRACK, false>(pend, __funnelshift_l(prv, cur, 1), c[1], 1, need, u0, S);
     if (KMAIN >= 2) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 2), c[2], 2, need, u0, S);
     if (KMAIN >= 3) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 4), c[3], 3, need, u0, S);
     if (KMAIN >= 4) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 8), c[4], 4, need, u0, S);
+    if (KMAIN >= 5) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 16), c[5], 5, need, u0, S);
     return pend;
 }
 
-// Exponent passes over the tile (ring half at hb): thread t owns the four
+// Exponent passes over the tile (ring quarter at hb): thread t owns the four
 // consecutive words 4t..4t+3 (one LDS.128 plus the left neighbour).  EDGE
 // masks the scan range, TRACK records per-k least slots while this CTA
-// still lacks them.  Words left after KMAIN passes (~0.4%) finish in one
-// divergent step per warp.
+// still lacks them.  Words left after KMAIN passes (~0.02% for KMAIN = 5)
+// are queued for the next start phase.
 template <bool EDGE, bool TRACK, int KMAIN>
 __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint32_t hb,
-                                          uint64_t tb, uint32_t need, uint32_t (&c)[5],
+                                          uint64_t tb, uint32_t need, uint32_t (&c)[6],
                                           unsigned long long &scanned) {
     constexpr int W = kWordsPerThread;
     const uint32_t w0 = W * threadIdx.x;
@@ -326,17 +347,13 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
         any |= left[i];
     }
     if (!EDGE) scanned += 32 * W;
-    if (__any_sync(0xffffffffu, any)) {
+    if (any) {
 #pragma unroll
         for (int i = 0; i < W; ++i) {
             if (!left[i]) continue;
             const uint64_t u0 = tb + 32ull * (w0 + i);
-            if (KMAIN == 4) {
-#ifdef SQF2K_EXP_NO_DEFER
-                const uint32_t e = kResCap;
-#else
+            if (KMAIN == 5) {
                 const uint32_t e = atomicAdd(&S.n_res, 1u);
-#endif
                 if (e < (uint32_t)kResCap) {  // deferred to the next start phase
                     S.res_w[e] = w0 + i;
                     S.res_p[e] = left[i];
@@ -345,7 +362,7 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
                                  P.esc, P.esc_count, P.esc_cap, P.fail, P.fail_count,
                                  P.fail_cap);
                 }
-            } else if (P.k_max > P.k_eff) {  // k_eff = KMAIN < 4: leftovers leave the tile
+            } else if (P.k_max > P.k_eff) {  // k_eff = KMAIN < 5: leftovers leave the tile
                 spill_word(left[i], u0, P.base_n, P.esc, P.esc_count, P.esc_cap);
             } else {
                 spill_word(left[i], u0, P.base_n, P.fail, P.fail_count, P.fail_cap);
@@ -368,12 +385,13 @@ __device__ __forceinline__ void drain_residue(TileSmem &S, const TileParams &P) 
     }
 }
 
-// KMAIN = min(k_eff, 4) unconditional passes; the export form ignores it.
+// KMAIN = min(k_eff, 5) unconditional passes; the export form ignores it.
 // Per tile: [start words from the pattern] | [scatter the medium and bucket
 // primes' hits as atomic bit clears] | [scan] -- three barriers, two in
 // export mode.
 template <bool FUSED, int KMAIN>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TileParams P) {
+    static_assert(kWordsPerThread == 4, "init_words and scan_tile own 4 words per thread");
     extern __shared__ __align__(16) uint8_t smem_raw[];
     TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
     const uint32_t G = gridDim.x;
@@ -391,16 +409,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     const uint32_t ti0 = (uint32_t)((lo_edge + kTile - 1) / kTile);
     const uint32_t ti1 = (uint32_t)(P.U / kTile);
 
-    // medium primes: q, kTile mod q and the first hit at the chunk base b0
+    // medium primes: each lane's descriptors, first hits at the chunk base b0
     const uint64_t b0 = pre ? (uint64_t)t0 * kTile - H : (uint64_t)t0 * kTile;
-    for (uint32_t m = threadIdx.x; m < P.n_med; m += kThreads) {
-        const uint32_t q = __ldg(&P.med[2 * m]);
-        const uint32_t r = (uint32_t)slot_residue(P.base_n, q);
-        const uint32_t bm = (uint32_t)(b0 % q);
-        S.med_q[m] = q;
-        S.med_tq[m] = __ldg(&P.med[2 * m + 1]);
-        S.off[m] = r >= bm ? r - bm : r + q - bm;
-    }
+    MedLane L;
+    init_medium(L, P, b0);
     if (threadIdx.x <= kDepthMax) {
         S.first[threadIdx.x] = ~0ull;
         S.cnt[threadIdx.x] = 0;
@@ -410,39 +422,34 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         S.n_res = 0;
     }
     uint32_t pbase = (uint32_t)((b0 / 32) % kPatWords);
+    const uint32_t ring_addr = smem_addr(S.ring);
 
     // the halo just below tile t0: the tail of quarter (t0 - 1) & 3
-    const uint32_t halo_at = ((t0 & 3u) * kTileWords + kRingWords - HW) & (kRingWords - 1);
+    const uint32_t halo_at = ((t0 + 3u) & 3u) * kTileWords + kTileWords - HW;
     if (FUSED) {
         if (pre) {  // pre-tile: sieve the H slots below the chunk
             init_halo(S.ring, halo_at, HW, b0, pbase, P);
             __syncthreads();
-            scatter_medium(S.ring, halo_at, S.off, S.med_q, P.tasks, P.task_beg, H);
-            scatter_bucket(S.ring, halo_at, P, t0 - 1, kTile - H);
-            __syncthreads();
-            for (uint32_t m = threadIdx.x; m < P.n_med; m += kThreads) {
-                const uint32_t o = S.off[m] - H % S.med_q[m];
-                S.off[m] = min(o, o + S.med_q[m]);
-            }
+            scatter_medium(L, ring_addr + 4 * halo_at, H);
+            scatter_bucket(ring_addr + 4 * halo_at, P, t0 - 1, kTile - H);
             pbase += HW;
             if (pbase >= kPatWords) pbase -= kPatWords;
         } else {
-            for (uint32_t i = threadIdx.x; i < HW; i += kThreads)
-                S.ring[(halo_at + i) & (kRingWords - 1)] = 0u;
+            for (uint32_t i = threadIdx.x; i < HW; i += kThreads) S.ring[halo_at + i] = 0u;
         }
     }
-    // S.n_res / S.cnt / S.first must be visible before the first start
-    // phase drains the (empty) residue queue
+    // S.n_res / S.cnt / S.first (and the halo) must be visible before the
+    // first start phase drains the (empty) residue queue
     __syncthreads();
 
-    uint32_t c[5] = {0, 0, 0, 0, 0};
+    uint32_t c[6] = {0, 0, 0, 0, 0, 0};
     unsigned long long scanned = 0;
     for (uint32_t t = t0; t < t1; ++t) {
         const uint64_t tb = (uint64_t)t * kTile;
         const uint32_t hb = (t & 3u) * kTileWords;
         const bool edge = t < ti0 || t >= ti1;
         // ---- start: pattern words (+ the previous tile's deferred words) ----
-        if (FUSED && KMAIN == 4) drain_residue(S, P);
+        if (FUSED && KMAIN == 5) drain_residue(S, P);
         if (edge) init_words<kTileWords, true>(S.ring, hb, tb, pbase, P);
         else init_words<kTileWords, false>(S.ring, hb, tb, pbase, P);
         pbase += kTileWords;
@@ -461,20 +468,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             S.res_tb = tb;
         }
 #ifndef SQF2K_EXP_NO_SCATTER
-        scatter_medium(S.ring, hb, S.off, S.med_q, P.tasks, P.task_beg, kTile);
-        scatter_bucket(S.ring, hb, P, t, 0);
+        scatter_medium(L, ring_addr + 4 * hb, kTile);
+        scatter_bucket(ring_addr + 4 * hb, P, t, 0);
 #endif
         __syncthreads();
-        advance_offsets(S.off, S.med_q, S.med_tq, P.n_med);
         if (!FUSED) {
-            for (uint32_t w = threadIdx.x; w < kTileWords; w += kThreads)
-                P.bits_out[(uint64_t)t * kTileWords + w] = S.ring[hb + w];
-            continue;  // the next start writes another quarter; its barrier orders the offsets
+            const uint4 v = *reinterpret_cast<const uint4 *>(&S.ring[hb + 4 * threadIdx.x]);
+            *reinterpret_cast<uint4 *>(&P.bits_out[(uint64_t)t * kTileWords + 4 * threadIdx.x]) = v;
+            continue;  // the next start writes another quarter
         }
         // ---- exponent passes (search.py:368-381) over the packed tile ----
         const uint32_t need = S.need;
 #ifndef SQF2K_EXP_NO_SCAN
-        if (need & 0x1eu) {
+        if (need & 0x3eu) {
             if (edge) scan_tile<true, true, KMAIN>(S, P, hb, tb, need, c, scanned);
             else scan_tile<false, true, KMAIN>(S, P, hb, tb, need, c, scanned);
         } else {
@@ -486,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     }
 
     if (FUSED) {  // the last tile's deferred words, then this CTA's minima
-        if (KMAIN == 4) drain_residue(S, P);
+        if (KMAIN == 5) drain_residue(S, P);
         __syncthreads();
         if (threadIdx.x >= 1 && threadIdx.x <= kDepthMax) {
             const unsigned long long f = S.first[threadIdx.x];
@@ -495,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         }
         const int lane = threadIdx.x & 31;
 #pragma unroll
-        for (int k = 2; k <= 4; ++k) {
+        for (int k = 2; k <= 5; ++k) {
             const uint32_t s = __reduce_add_sync(0xffffffffu, c[k]);
             if (lane == 0 && s) atomicAdd(&P.hist[k], (unsigned long long)s);
         }
@@ -503,83 +509,79 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
 #pragma unroll
         for (int d = 16; d >= 1; d >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, d);
         if (lane == 0 && sc) atomicAdd(P.scanned, sc);
-        if (threadIdx.x >= 5 && threadIdx.x <= kDepthMax && S.cnt[threadIdx.x])
+        if (threadIdx.x >= 6 && threadIdx.x <= kDepthMax && S.cnt[threadIdx.x])
             atomicAdd(&P.hist[threadIdx.x], (unsigned long long)S.cnt[threadIdx.x]);
     }
 }
 
 // -------------------------------------------------------------------------
-// Medium-prime tables (q, kTile mod q) and the scatter tasks, built on the
-// host from the table's primes in [11, kPMed) and cached on the device per
-// set.  A prime with h = kTile/q hits per tile and h >= 16 is swept by whole
-// warps (S sweeps of ~kItemHits hits per lane: lane l starts at hit l + 32s,
-// step 32*S*q); a rarer prime is split into ~kItemHits-hit items (start j,
-// step parts*q).  Descriptors sorted by trip count fill 32-lane tasks, and the
-// tasks go to the kThreads/32 warps longest-first.
+// Medium-prime scatter schedule, built on the host from the table's primes in
+// [11, kPMed) and cached on the device per set.  A prime with h = kTile/q
+// hits per tile (q = p^2) and h >= 16 is swept by whole warps (S sweeps of
+// ~item hits per lane: lane l starts at hit l + 32s, step 32*S*q); a rarer
+// prime is split into ~item-hit descriptors (start j, step parts*q).
+// Descriptors sorted by trip count fill 32-lane tasks, and the tasks go to
+// the kThreads/32 warps longest-first, at most kTaskSlots per warp (the
+// item size grows until they fit).
 struct MedTables {
-    std::vector<uint32_t> med;
-    std::vector<uint32_t> tasks;  // (x, y) pairs, 32 per task, ordered by warp
-    std::vector<uint32_t> beg;    // warp w runs tasks [beg[w], beg[w+1])
-    uint32_t n_med = 0, n_tasks = 0;
+    std::vector<uint32_t> q;      // p^2 per medium prime
+    std::vector<uint32_t> tasks;  // (x, y) pairs: [warp][kTaskSlots][lane]
+    uint32_t n_tasks = 0;
 };
 
 MedTables build_med(const std::vector<uint32_t> &med_primes) {
-    MedTables t;
+    constexpr int kWarps = kThreads / 32;
     struct Desc {
         double trips;
         uint32_t x, y;
     };
-    std::vector<Desc> descs;
-    for (uint32_t p : med_primes) {
-        if (t.n_med >= (uint32_t)kMaxMed) break;
-        const uint32_t q = p * p, m = t.n_med;
-        t.med.push_back(q);
-        t.med.push_back((uint32_t)kTile % q);
-        const double h = (double)kTile / q;
-        if (h >= 16.0) {
-            uint32_t S = (uint32_t)(h / (32.0 * kItemHits) + 0.5);
-            S = std::max<uint32_t>(1, S);
-            for (uint32_t sw = 0; sw < S; ++sw)
-                for (uint32_t l = 0; l < 32; ++l)
-                    descs.push_back({h / (32.0 * S) + 1.0, m | ((l + 32 * sw) << 8), 32 * S * q});
-        } else {
-            uint32_t parts = std::max<uint32_t>(1, (uint32_t)(h / kItemHits + 0.5));
-            for (uint32_t j = 0; j < parts; ++j)
-                descs.push_back({h / parts + 1.0, m | (j << 8), parts * q});
+    for (double item = kItemHits;; item *= 1.5) {
+        MedTables t;
+        std::vector<Desc> descs;
+        for (uint32_t p : med_primes) {
+            if (t.q.size() >= (size_t)kMaxMed) break;
+            const uint32_t q = p * p, m = (uint32_t)t.q.size();
+            t.q.push_back(q);
+            const double h = (double)kTile / q;
+            if (h >= 16.0) {
+                const uint32_t S = std::max<uint32_t>(1, (uint32_t)(h / (32.0 * item) + 0.5));
+                for (uint32_t sw = 0; sw < S; ++sw)
+                    for (uint32_t l = 0; l < 32; ++l)
+                        descs.push_back({h / (32.0 * S) + 1.0, m | ((l + 32 * sw) << 8), 32 * S * q});
+            } else {
+                const uint32_t parts = std::max<uint32_t>(1, (uint32_t)(h / item + 0.5));
+                for (uint32_t j = 0; j < parts; ++j)
+                    descs.push_back({h / parts + 1.0, m | (j << 8), parts * q});
+            }
         }
-        ++t.n_med;
-    }
-    std::stable_sort(descs.begin(), descs.end(),
-                     [](const Desc &a, const Desc &b) { return a.trips > b.trips; });
-    const uint32_t n_tasks = (uint32_t)((descs.size() + 31) / 32);
-    std::vector<double> cost(n_tasks, 0.0);
-    for (uint32_t k = 0; k < n_tasks; ++k) cost[k] = descs[32 * k].trips + 1.0;  // + task overhead
-    constexpr int kWarps = kThreads / 32;
-    std::vector<double> load(kWarps, 0.0);
-    std::vector<std::vector<uint32_t>> per_warp(kWarps);
-    for (uint32_t k = 0; k < n_tasks; ++k) {  // tasks are already longest-first
-        const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-        load[w] += cost[k];
-        per_warp[w].push_back(k);
-    }
-    t.beg.push_back(0);
-    for (int w = 0; w < kWarps; ++w) {
-        for (uint32_t k : per_warp[w])
+        std::stable_sort(descs.begin(), descs.end(),
+                         [](const Desc &a, const Desc &b) { return a.trips > b.trips; });
+        const uint32_t n_tasks = (uint32_t)((descs.size() + 31) / 32);
+        if (n_tasks > (uint32_t)(kWarps * kTaskSlots)) continue;
+        std::vector<double> load(kWarps, 0.0);
+        std::vector<int> used(kWarps, 0);
+        t.tasks.assign((size_t)kWarps * kTaskSlots * 64, 0u);  // step 0: idle lane
+        for (uint32_t k = 0; k < n_tasks; ++k) {  // longest first, least-loaded warp with room
+            int w = -1;
+            for (int i = 0; i < kWarps; ++i)
+                if (used[i] < kTaskSlots && (w < 0 || load[i] < load[w])) w = i;
+            load[w] += descs[32 * k].trips / 2.0 + 2.0;  // two clears per trip + task overhead
+            const size_t at = ((size_t)w * kTaskSlots + used[w]++) * 64;
             for (uint32_t l = 0; l < 32; ++l) {
                 const uint32_t i = 32 * k + l;
-                t.tasks.push_back(i < descs.size() ? descs[i].x : 0u);
-                t.tasks.push_back(i < descs.size() ? descs[i].y : 0u);  // step 0: idle lane
+                if (i >= descs.size()) break;
+                t.tasks[at + 2 * l] = descs[i].x;
+                t.tasks[at + 2 * l + 1] = descs[i].y;
             }
-        t.beg.push_back((uint32_t)(t.tasks.size() / 64));
+        }
+        t.n_tasks = n_tasks;
+        return t;
     }
-    t.n_tasks = n_tasks;
-    return t;
 }
 
 struct MedCache {
     std::vector<uint32_t> key;
-    uint32_t n_med = 0, n_tasks = 0;
-    DevBuf buf;
+    DevBuf buf;  // kMaxMed q values, then the task table
 };
 
 MedCache g_med;  // the library serialises calls
@@ -620,26 +622,21 @@ void run_tile_batch(const BatchArgs &a) {
     const uint32_t n_tiles = (uint32_t)ceil_div(a.U, kTile);
 
     // medium tables: cached per distinct prime set
-    constexpr int kWarps = kThreads / 32;
+    constexpr size_t kTaskWords = (size_t)(kThreads / 32) * kTaskSlots * 64;
     if (g_med.key != *a.med_primes || !g_med.buf.ptr) {
         MedTables t = build_med(*a.med_primes);
-        if (t.n_tasks > (uint32_t)kMaxTasks) throw Error{SQF2K_ECUDA, "medium task table overflow"};
         g_med.key = *a.med_primes;
-        g_med.n_med = t.n_med;
-        g_med.n_tasks = t.n_tasks;
-        const size_t words = 2 * kMaxMed + 64 * kMaxTasks + kWarps + 1;
-        g_med.buf.reserve(words * 4);
-        std::vector<uint32_t> host(words, 0);
-        std::copy(t.med.begin(), t.med.end(), host.begin());
-        std::copy(t.tasks.begin(), t.tasks.end(), host.begin() + 2 * kMaxMed);
-        std::copy(t.beg.begin(), t.beg.end(), host.begin() + 2 * kMaxMed + 64 * kMaxTasks);
+        g_med.buf.reserve((kMaxMed + kTaskWords) * 4);
+        std::vector<uint32_t> host(kMaxMed + kTaskWords, 0);
+        std::copy(t.q.begin(), t.q.end(), host.begin());
+        std::copy(t.tasks.begin(), t.tasks.end(), host.begin() + kMaxMed);
         SQF2K_CUDA(cudaMemcpy(g_med.buf.ptr, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
         dev_alloc_bump();  // captured graphs read this table
     }
 
     // p = 3, 5, 7 pattern of this domain
-    c.pattern.reserve(kPatWords * 4);
-    launch("pattern", pattern_kernel, dim3(ceil_div(kPatWords, 256)), dim3(256), 0, a.base_n,
+    c.pattern.reserve((kPatWords + kTileWords) * 4);
+    launch("pattern", pattern_kernel, dim3(ceil_div(kPatWords + kTileWords, 256)), dim3(256), 0, a.base_n,
            a.pattern_present, c.pattern.as<uint32_t>());
 
     // bucket lists (sizes bounded on the host: no sync)
@@ -682,12 +679,10 @@ void run_tile_batch(const BatchArgs &a) {
     P.n_tiles = n_tiles;
     P.k_eff = a.k_eff;
     P.k_max = a.k_max;
-    P.n_med = g_med.n_med;
 
     P.pattern = c.pattern.as<uint32_t>();
     P.med = g_med.buf.as<uint32_t>();
-    P.tasks = reinterpret_cast<const uint2 *>(g_med.buf.as<uint32_t>() + 2 * kMaxMed);
-    P.task_beg = g_med.buf.as<uint32_t>() + 2 * kMaxMed + 64 * kMaxTasks;
+    P.tasks = reinterpret_cast<const uint2 *>(g_med.buf.as<uint32_t>() + kMaxMed);
     P.tile_start = tile_start;
     P.tile_count = counts;
     P.hits = c.hits.as<uint16_t>();
@@ -707,11 +702,12 @@ void run_tile_batch(const BatchArgs &a) {
     if (const char *g = std::getenv("SQF2K_DEBUG_GRID")) grid_cap = std::max(1, atoi(g));
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(n_tiles, grid_cap));
     if (a.fused) {
-        const uint32_t kmain = std::min<uint32_t>(a.k_eff, 4);
+        const uint32_t kmain = std::min<uint32_t>(a.k_eff, 5);
         if (kmain == 1) launch_tile<true, 1>("tile_fused", grid, smem, P);
         else if (kmain == 2) launch_tile<true, 2>("tile_fused", grid, smem, P);
         else if (kmain == 3) launch_tile<true, 3>("tile_fused", grid, smem, P);
-        else launch_tile<true, 4>("tile_fused", grid, smem, P);
+        else if (kmain == 4) launch_tile<true, 4>("tile_fused", grid, smem, P);
+        else launch_tile<true, 5>("tile_fused", grid, smem, P);
     } else {
         launch_tile<false, 1>("tile_export", grid, smem, P);
     }

@@ -4,24 +4,19 @@
 // integers n(u) = base_n + 2u (base_n odd, possibly <= 0; n < 1 reads as
 // "not squarefree", search.py:282-286).  Tiles are kTile consecutive slots.
 //
-// Per tile a CTA
-//   1. holds one byte per slot (1 = squarefree so far) and stores 0 at every
-//      odd multiple of p^2 for the medium primes 11 <= p < kPMed (balanced
-//      "items" of <= ~9 hits, per-CTA incremental offsets, no divisions) and
-//      for the bucket primes p >= kPMed (hit lists precomputed per tile in HBM);
-//   2. packs the bytes into 32-bit LSB-first words and ANDs in the periodic
-//      pattern of p = 3, 5, 7 (one table word per u-word mod 9*25*49);
+// Per tile a CTA sieves the tile directly in packed form (one bit per odd
+// slot, 32-bit LSB-first words in shared memory):
+//   1. each word starts as the periodic mask of p = 3, 5, 7 (one table word
+//      per u-word mod 9*25*49);
+//   2. the odd multiples of p^2 are cleared with shared-memory atomic ANDs --
+//      medium primes 11 <= p < kPMed from per-lane "descriptors" whose next
+//      hit offset lives in a register across tiles (no division, no table
+//      walk), bucket primes p >= kPMed from per-tile hit lists in HBM;
 //   3. fused mode: runs the exponent passes k = 1..k_eff of search.py:368-381
-//      over the packed words -- passes 1..4 unconditionally for every word
-//      (funnel shifts of the word and its left neighbour), the rare remainder
-//      divergently -- reading n - 2^k from the tile or the rolled halo of the
-//      previous tile (2^(k_eff-1) slots); export mode: stores the words.
-//
-// Bytes are laid out so that packing 32 slots is two conflict-free LDS.128
-// and seven shift-or's: within each 1024-slot block, slot s (local) lives at
-//   ((s>>3)&3) | ((s&3)<<2) | (((s>>5)&31)<<4) | (((s>>2)&1)<<9)
-// i.e. the 32-bit word x_i (i = s&7) of a 32-slot group holds the slots
-// 8j+i in its bytes j, so  word = OR_i x_i << i.
+//      over the words -- passes 1..5 unconditionally for every word (funnel
+//      shifts of the word and its left neighbour), the rare remainder
+//      divergently -- reading n - 2^k from the tile or the previous tile's
+//      tail (2^(k_eff-1) slots of halo); export mode: stores the words.
 #pragma once
 
 #include <stdint.h>
@@ -50,7 +45,7 @@ constexpr int kHaloMax = 1 << (kDepthMax - 1);
 constexpr int kHaloWordsMax = kHaloMax / 32;
 constexpr uint32_t kPMed = 1024;        // medium primes: 11 <= p < kPMed
 constexpr int kMaxMed = 176;            // pi(1023) - 4 = 168
-constexpr int kMaxTasks = 256;          // 32-lane scatter tasks per medium set
+constexpr int kTaskSlots = 4;           // 32-lane scatter tasks per warp (registers)
 constexpr int kItemHits = 4;            // target hits per lane per tile
 constexpr uint32_t kPatWords = 9 * 25 * 49;  // period of the p = 3, 5, 7 pattern in words
 constexpr int kResCap = 256;           // deferred residue words per tile
@@ -90,11 +85,10 @@ struct TileParams {
     uint32_t n_tiles;
     uint32_t k_eff;      // passes inside the tile
     uint32_t k_max;      // run limit: escalate when k_max > k_eff
-    uint32_t n_med;
-    const uint32_t *pattern;     // kPatWords words of the p = 3, 5, 7 mask, by u-word
-    const uint32_t *med;         // per medium prime: q, kTile mod q          (2 x n_med)
-    const uint2 *tasks;          // 32 lane descriptors (m | mult << 8, step) per task
-    const uint32_t *task_beg;    // warp w runs tasks [task_beg[w], task_beg[w+1])
+    const uint32_t *pattern;     // p = 3, 5, 7 mask by u-word mod kPatWords (+ kTileWords
+                                 // repeated words, so a tile never wraps)
+    const uint32_t *med;         // q = p^2 of the medium primes
+    const uint2 *tasks;          // [warp][kTaskSlots][lane]: (m | mult << 8, step), step 0 idle
     const uint32_t *tile_start;  // exact bucket lists: bounds, n_tiles + 1 (or null)
     const uint32_t *tile_count;  // fixed-capacity lists: hits of tile t at t*kBucketCap
     const uint16_t *hits;        // bucket hits, offsets within the tile
@@ -109,11 +103,6 @@ struct TileParams {
     unsigned long long *scanned; // fused mode: odd n entering the scan (hist[1] by conservation)
     uint32_t *bits_out;          // export mode: packed words of the domain
 };
-
-__device__ __forceinline__ uint32_t byte_pos(uint32_t s) {
-    return (s & ~1023u) | ((s >> 3) & 3u) | ((s & 3u) << 2) | ((s >> 1) & 0x1f0u) |
-           ((s << 7) & 0x200u);
-}
 
 // residue of the first slot u >= 0 with q | base_n + 2u, i.e. u = -base_n/2 mod q
 __device__ __host__ __forceinline__ uint64_t slot_residue(int64_t base_n, uint64_t q) {
