@@ -121,11 +121,10 @@ struct TileSmem {
     unsigned long long first[kDepthMax + 1];
     uint32_t cnt[kDepthMax + 1];  // counts of k >= 6 (rare)
     uint32_t need;
-    // words left after the main passes of the last scanned tile, finished
-    // during the next start phase
-    uint32_t res_w[kResCap], res_p[kResCap];
-    uint32_t n_res, res_hb;
-    unsigned long long res_tb;
+    // words left after the main passes of tile t (queue t & 1), finished
+    // while tile t + 1 is scanned
+    uint32_t res_w[2][kResCap], res_p[2][kResCap];
+    uint32_t n_res[2];
 };
 
 // Clear slot o of the words starting at shared address wbase (byte address
@@ -188,9 +187,12 @@ __device__ __forceinline__ void init_medium(MedLane &L, const TileParams &P, uin
     }
 }
 
-// clear the bucket hits of tile t with offsets in [skip, kTile), shifted by -skip
+// clear the bucket hits of tile t with offsets in [skip, kTile), shifted by
+// -skip; run by the last warp only (~5 hits per tile; build_med gives that
+// warp less medium work)
 __device__ __forceinline__ void scatter_bucket(uint32_t wbase, const TileParams &P, uint32_t t,
                                                uint32_t skip) {
+    if ((threadIdx.x >> 5) != kThreads / 32 - 1) return;
     uint32_t b, e;
     if (P.tile_start) {
         b = __ldg(&P.tile_start[t]);
@@ -199,8 +201,7 @@ __device__ __forceinline__ void scatter_bucket(uint32_t wbase, const TileParams 
         b = t * (uint32_t)kBucketCap;
         e = b + min(__ldg(&P.tile_count[t]), (uint32_t)kBucketCap);
     }
-    // last threads first: the task balance leaves them no lighter than others
-    for (uint32_t i = b + (kThreads - 1 - threadIdx.x); i < e; i += kThreads) {
+    for (uint32_t i = b + (threadIdx.x & 31); i < e; i += 32) {
         const uint32_t o = __ldg(&P.hits[i]);
         if (o >= skip) clear_bit(wbase, o - skip);
     }
@@ -258,13 +259,9 @@ __device__ __noinline__ void spill_word(uint32_t pend, uint64_t u0, int64_t base
 }
 
 // Passes k = 6..k_eff for one word (divergent, rare: ~0.02% of words).
-__device__ __noinline__ void scan_residue(TileSmem &S, uint32_t hb, uint32_t w, uint64_t u0,
-                                          uint32_t pend, uint32_t need, uint32_t k_eff,
-                                          uint32_t k_max, int64_t base_n, unsigned long long *esc,
-                                          unsigned long long *esc_count, uint64_t esc_cap,
-                                          unsigned long long *fail,
-                                          unsigned long long *fail_count, uint64_t fail_cap) {
-    for (uint32_t k = 6; k <= k_eff && pend; ++k) {
+__device__ __forceinline__ void scan_residue(TileSmem &S, const TileParams &P, uint32_t hb,
+                                             uint32_t w, uint64_t u0, uint32_t pend, uint32_t need) {
+    for (uint32_t k = 6; k <= P.k_eff && pend; ++k) {
         const uint32_t sl = S.ring[(hb + w - (1u << (k - 6))) & (kRingWords - 1)];
         const uint32_t nw = pend & sl;
         if (nw) {
@@ -274,8 +271,8 @@ __device__ __noinline__ void scan_residue(TileSmem &S, uint32_t hb, uint32_t w, 
         pend &= ~sl;
     }
     if (pend) {
-        if (k_max > k_eff) spill_word(pend, u0, base_n, esc, esc_count, esc_cap);
-        else spill_word(pend, u0, base_n, fail, fail_count, fail_cap);
+        if (P.k_max > P.k_eff) spill_word(pend, u0, P.base_n, P.esc, P.esc_count, P.esc_cap);
+        else spill_word(pend, u0, P.base_n, P.fail, P.fail_count, P.fail_cap);
     }
 }
 
@@ -314,7 +311,7 @@ __device__ __forceinline__ uint32_t scan_word(uint32_t pend, uint32_t prv, uint3
 template <bool EDGE, bool TRACK, int KMAIN>
 __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint32_t hb,
                                           uint64_t tb, uint32_t need, uint32_t (&c)[6],
-                                          unsigned long long &scanned) {
+                                          uint32_t &scanned, uint32_t qi) {
     constexpr int W = kWordsPerThread;
     const uint32_t w0 = W * threadIdx.x;
     uint32_t cur[W], prv[W];
@@ -353,14 +350,12 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
             if (!left[i]) continue;
             const uint64_t u0 = tb + 32ull * (w0 + i);
             if (KMAIN == 5) {
-                const uint32_t e = atomicAdd(&S.n_res, 1u);
-                if (e < (uint32_t)kResCap) {  // deferred to the next start phase
-                    S.res_w[e] = w0 + i;
-                    S.res_p[e] = left[i];
+                const uint32_t e = atomicAdd(&S.n_res[qi], 1u);
+                if (e < (uint32_t)kResCap) {  // deferred to the next tile's scan phase
+                    S.res_w[qi][e] = w0 + i;
+                    S.res_p[qi][e] = left[i];
                 } else {
-                    scan_residue(S, hb, w0 + i, u0, left[i], need, P.k_eff, P.k_max, P.base_n,
-                                 P.esc, P.esc_count, P.esc_cap, P.fail, P.fail_count,
-                                 P.fail_cap);
+                    scan_residue(S, P, hb, w0 + i, u0, left[i], need);
                 }
             } else if (P.k_max > P.k_eff) {  // k_eff = KMAIN < 5: leftovers leave the tile
                 spill_word(left[i], u0, P.base_n, P.esc, P.esc_count, P.esc_cap);
@@ -371,27 +366,30 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
     }
 }
 
-// Finish the deferred words of the last scanned tile (its ring quarter and
-// the halo below stay intact while the next tile starts in another quarter).
-// Entries are spread over the warps so no warp carries them all.
-__device__ __forceinline__ void drain_residue(TileSmem &S, const TileParams &P) {
-    const uint32_t n = min(S.n_res, (uint32_t)kResCap);
-    if (!n) return;
-    const uint32_t e = (threadIdx.x & 31) * (kThreads / 32) + (threadIdx.x >> 5);
-    if (e < n) {
-        const uint32_t w = S.res_w[e];
-        scan_residue(S, S.res_hb, w, S.res_tb + 32ull * w, S.res_p[e], S.need, P.k_eff, P.k_max,
-                     P.base_n, P.esc, P.esc_count, P.esc_cap, P.fail, P.fail_count, P.fail_cap);
+// Finish the deferred words of tile tp (queue tp & 1; its ring quarter and
+// the halo below stay intact until tile tp + 3 starts).  One warp per tile,
+// rotating, so no warp carries them all.
+__device__ __forceinline__ void drain_residue(TileSmem &S, const TileParams &P, uint32_t tp,
+                                              uint32_t need) {
+    if ((threadIdx.x >> 5) != (tp & (kThreads / 32 - 1))) return;
+    const uint32_t qi = tp & 1u, n = min(S.n_res[qi], (uint32_t)kResCap);
+    const uint32_t hb = (tp & 3u) * kTileWords;
+    for (uint32_t e = threadIdx.x & 31; e < n; e += 32) {
+        const uint32_t w = S.res_w[qi][e];
+        scan_residue(S, P, hb, w, (uint64_t)tp * kTile + 32ull * w, S.res_p[qi][e], need);
     }
 }
 
 // KMAIN = min(k_eff, 5) unconditional passes; the export form ignores it.
-// Per tile: [start words from the pattern] | [scatter the medium and bucket
-// primes' hits as atomic bit clears] | [scan] -- three barriers, two in
-// export mode.
+// Per tile t, two phases between barriers:
+//   X(t): clear the medium and bucket primes' hits in quarter t & 3;
+//   Y(t): scan tile t (fused) or store it (export), finish tile t - 1's
+//         deferred words, and start tile t + 1's words from the pattern in
+//         quarter (t + 1) & 3 -- nothing in Y(t) reads that quarter.
 template <bool FUSED, int KMAIN>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TileParams P) {
     static_assert(kWordsPerThread == 4, "init_words and scan_tile own 4 words per thread");
+    static_assert(kThreads / 32 == 8, "drain_residue rotates over 8 warps");
     extern __shared__ __align__(16) uint8_t smem_raw[];
     TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
     const uint32_t G = gridDim.x;
@@ -417,10 +415,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         S.first[threadIdx.x] = ~0ull;
         S.cnt[threadIdx.x] = 0;
     }
-    if (threadIdx.x == 0) {
-        S.need = ~0u;
-        S.n_res = 0;
-    }
+    if (threadIdx.x < 2) S.n_res[threadIdx.x] = 0;
+    if (threadIdx.x == 0) S.need = ~0u;
     uint32_t pbase = (uint32_t)((b0 / 32) % kPatWords);
     const uint32_t ring_addr = smem_addr(S.ring);
 
@@ -438,61 +434,64 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             for (uint32_t i = threadIdx.x; i < HW; i += kThreads) S.ring[halo_at + i] = 0u;
         }
     }
-    // S.n_res / S.cnt / S.first (and the halo) must be visible before the
-    // first start phase drains the (empty) residue queue
+    {  // tile t0's words
+        const uint64_t tb = (uint64_t)t0 * kTile, hb = (t0 & 3u) * kTileWords;
+        if (t0 < ti0 || t0 >= ti1) init_words<kTileWords, true>(S.ring, hb, tb, pbase, P);
+        else init_words<kTileWords, false>(S.ring, hb, tb, pbase, P);
+        pbase += kTileWords;
+        if (pbase >= kPatWords) pbase -= kPatWords;
+    }
     __syncthreads();
 
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
-    unsigned long long scanned = 0;
+    uint32_t scanned = 0;  // <= 128 per tile, < 2^21 tiles
     for (uint32_t t = t0; t < t1; ++t) {
         const uint64_t tb = (uint64_t)t * kTile;
         const uint32_t hb = (t & 3u) * kTileWords;
         const bool edge = t < ti0 || t >= ti1;
-        // ---- start: pattern words (+ the previous tile's deferred words) ----
-        if (FUSED && KMAIN == 5) drain_residue(S, P);
-        if (edge) init_words<kTileWords, true>(S.ring, hb, tb, pbase, P);
-        else init_words<kTileWords, false>(S.ring, hb, tb, pbase, P);
-        pbase += kTileWords;
-        if (pbase >= kPatWords) pbase -= kPatWords;
+        // ---- X(t): clear the odd multiples of p^2, p >= 11 ----
         // S.first[k] keeps this CTA's least slot with exponent k (slots grow
-        // with t, so the first tile where k shows up holds it); stop tracking
-        // a k once it is known.  S.first is never reset, so the deferred
-        // residue words (atomicMin in this phase) cannot race this.
+        // with t and residue words finish in tile order); stop tracking a k
+        // once it is known.  S.first is never reset.
         if (FUSED && threadIdx.x >= 1 && threadIdx.x <= kDepthMax && S.first[threadIdx.x] != ~0ull)
             atomicAnd(&S.need, ~(1u << threadIdx.x));
-        __syncthreads();
-        // ---- sieve: clear the odd multiples of p^2, p >= 11 ----
-        if (FUSED && threadIdx.x == 0) {
-            S.n_res = 0;
-            S.res_hb = hb;
-            S.res_tb = tb;
-        }
+        if (FUSED && threadIdx.x == 0) S.n_res[t & 1u] = 0;  // tile t - 2's queue is done
 #ifndef SQF2K_EXP_NO_SCATTER
         scatter_medium(L, ring_addr + 4 * hb, kTile);
         scatter_bucket(ring_addr + 4 * hb, P, t, 0);
 #endif
         __syncthreads();
+        // ---- Y(t) ----
+        const bool more = t + 1 < t1;
+        const bool edge1 = t + 1 < ti0 || t + 1 >= ti1;
         if (!FUSED) {
             const uint4 v = *reinterpret_cast<const uint4 *>(&S.ring[hb + 4 * threadIdx.x]);
             *reinterpret_cast<uint4 *>(&P.bits_out[(uint64_t)t * kTileWords + 4 * threadIdx.x]) = v;
-            continue;  // the next start writes another quarter
-        }
-        // ---- exponent passes (search.py:368-381) over the packed tile ----
-        const uint32_t need = S.need;
-#ifndef SQF2K_EXP_NO_SCAN
-        if (need & 0x3eu) {
-            if (edge) scan_tile<true, true, KMAIN>(S, P, hb, tb, need, c, scanned);
-            else scan_tile<false, true, KMAIN>(S, P, hb, tb, need, c, scanned);
         } else {
-            if (edge) scan_tile<true, false, KMAIN>(S, P, hb, tb, need, c, scanned);
-            else scan_tile<false, false, KMAIN>(S, P, hb, tb, need, c, scanned);
-        }
+            const uint32_t need = S.need;
+#ifndef SQF2K_EXP_NO_SCAN
+            if (need & 0x3eu) {
+                if (edge) scan_tile<true, true, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+                else scan_tile<false, true, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+            } else {
+                if (edge) scan_tile<true, false, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+                else scan_tile<false, false, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+            }
 #endif
+            if (KMAIN == 5 && t > t0) drain_residue(S, P, t - 1, need);
+        }
+        if (more) {
+            const uint32_t hb1 = ((t + 1) & 3u) * kTileWords;
+            if (edge1) init_words<kTileWords, true>(S.ring, hb1, tb + kTile, pbase, P);
+            else init_words<kTileWords, false>(S.ring, hb1, tb + kTile, pbase, P);
+            pbase += kTileWords;
+            if (pbase >= kPatWords) pbase -= kPatWords;
+        }
         __syncthreads();
     }
 
     if (FUSED) {  // the last tile's deferred words, then this CTA's minima
-        if (KMAIN == 5) drain_residue(S, P);
+        if (KMAIN == 5) drain_residue(S, P, t1 - 1, S.need);
         __syncthreads();
         if (threadIdx.x >= 1 && threadIdx.x <= kDepthMax) {
             const unsigned long long f = S.first[threadIdx.x];
@@ -505,9 +504,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             const uint32_t s = __reduce_add_sync(0xffffffffu, c[k]);
             if (lane == 0 && s) atomicAdd(&P.hist[k], (unsigned long long)s);
         }
-        unsigned long long sc = scanned;
-#pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, d);
+        const unsigned long long sc = __reduce_add_sync(0xffffffffu, scanned);
         if (lane == 0 && sc) atomicAdd(P.scanned, sc);
         if (threadIdx.x >= 6 && threadIdx.x <= kDepthMax && S.cnt[threadIdx.x])
             atomicAdd(&P.hist[threadIdx.x], (unsigned long long)S.cnt[threadIdx.x]);
@@ -559,6 +556,7 @@ MedTables build_med(const std::vector<uint32_t> &med_primes) {
         const uint32_t n_tasks = (uint32_t)((descs.size() + 31) / 32);
         if (n_tasks > (uint32_t)(kWarps * kTaskSlots)) continue;
         std::vector<double> load(kWarps, 0.0);
+        load[kWarps - 1] = 4.0;  // the bucket warp (scatter_bucket)
         std::vector<int> used(kWarps, 0);
         t.tasks.assign((size_t)kWarps * kTaskSlots * 64, 0u);  // step 0: idle lane
         for (uint32_t k = 0; k < n_tasks; ++k) {  // longest first, least-loaded warp with room

@@ -37,7 +37,7 @@ constexpr int kTileWords = kTile / 32;  // 1024 packed words
 constexpr int kWordsPerThread = SQF2K_WORDS_PER_THREAD;  // words per thread in pack and scan
 constexpr int kThreads = kTileWords / kWordsPerThread;  // CTA size
 #ifndef SQF2K_CTAS_PER_SM
-#define SQF2K_CTAS_PER_SM 4
+#define SQF2K_CTAS_PER_SM 6
 #endif
 constexpr int kCtasPerSm = SQF2K_CTAS_PER_SM;
 constexpr int kDepthMax = 16;           // max exponent resolved in-tile
