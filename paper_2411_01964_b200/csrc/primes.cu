@@ -23,60 +23,132 @@ constexpr int kSegWords = kSegOdds / 32;   // 2048 u32 words
 constexpr int kSieveThreads = 512;
 constexpr int kMaxBase = 6600;             // pi(65536) = 6542 >= pi(isqrt(2^32))
 
-// Split of a table holding every prime <= limit: positional (kPiPow2).
+__constant__ uint32_t c_pi_pow2[kClasses + 1] = SQF2K_PI_POW2;
+
+// Split of a table holding every prime <= limit: positional (pi(2^m)).
 __device__ void fill_info(PrimeInfo *info, unsigned long long n) {
     info->count = n;
     info->i_lo = (uint32_t)min(n, (unsigned long long)kPiBelowPMed);
     info->i_hi = (uint32_t)n;
-    for (int j = 0; j <= kClasses; ++j) info->cls[j] = (uint32_t)min(n, (unsigned long long)pi_pow2(j));
+#pragma unroll
+    for (int j = 0; j <= kClasses; ++j) info->cls[j] = (uint32_t)min(n, (unsigned long long)c_pi_pow2[j]);
 }
 
-// Whole table for limit < 2^17 (one segment) in one CTA: base primes, a byte
-// per odd candidate in shared memory (plain byte stores, no atomics), ordered
-// compaction and the split.
-__global__ void __launch_bounds__(kSieveThreads) prime_small_kernel(uint64_t limit,
+// Whole table for limit < 2^17 (at most 2048 words of odd candidates) in one
+// CTA of 1024 threads, a bit per odd candidate in shared memory: the ten odd
+// primes below 32 are applied per word as shifted periodic patterns (i0 mod
+// p by a multiply-high with a magic constant, exact for i0 < 2^16), the
+// larger base primes clear their multiples from p^2 with shared-memory
+// atomics spread over all threads (~7 per thread at limit 2^15).  Ordered
+// compaction: block scan, primes staged in shared memory, one coalesced
+// copy out.
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallStage = 12288;  // > pi(2^17) = 12251
+constexpr int kNumOddBase = 71;     // odd primes <= 361 = isqrt(2^17 - 1)
+__constant__ uint16_t c_odd_base[kNumOddBase] = {
+    3,   5,   7,   11,  13,  17,  19,  23,  29,  31,  37,  41,  43,  47,  53,  59,  61,  67,
+    71,  73,  79,  83,  89,  97,  101, 103, 107, 109, 113, 127, 131, 137, 139, 149, 151, 157,
+    163, 167, 173, 179, 181, 191, 193, 197, 199, 211, 223, 227, 229, 233, 239, 241, 251, 257,
+    263, 269, 271, 277, 281, 283, 293, 307, 311, 313, 317, 331, 337, 347, 349, 353, 359};
+// floor(2^32 / p) + 1: floor(i0 / p) = umulhi(i0, magic) for i0 < 2^16
+__constant__ uint32_t c_odd_magic[kNumOddBase] = {
+    1431655766u, 858993460u, 613566757u, 390451573u, 330382100u, 252645136u,
+    226050911u, 186737709u, 148102321u, 138547333u, 116080198u, 104755300u,
+    99882961u, 91382283u, 81037119u, 72796056u, 70409300u, 64103990u,
+    60492498u, 58835169u, 54366675u, 51746594u, 48258060u, 44278014u,
+    42524429u, 41698712u, 40139882u, 39403370u, 38008561u, 33818641u,
+    32786010u, 31350127u, 30899046u, 28825284u, 28443493u, 27356480u,
+    26349493u, 25718368u, 24826401u, 23994231u, 23729102u, 22486740u,
+    22253717u, 21801865u, 21582751u, 20355296u, 19259944u, 18920561u,
+    18755316u, 18433337u, 17970575u, 17821442u, 17111424u, 16711936u,
+    16330675u, 15966422u, 15848588u, 15505298u, 15284582u, 15176563u,
+    14658592u, 13990122u, 13810185u, 13721941u, 13548793u, 12975733u,
+    12744711u, 12377428u, 12306497u, 12167047u, 11963698u,
+};
+// bits 0, p, 2p, ... < 32 for the ten odd primes below 32
+__constant__ uint32_t c_odd_rep[10] = {0x49249249u, 0x42108421u, 0x10204081u, 0x400801u,
+                                       0x4002001u,  0x20001u,    0x80001u,    0x800001u,
+                                       0x20000001u, 0x80000001u};
+
+struct SmallTables {
+    uint32_t p[kNumOddBase], magic[kNumOddBase], rep[10];
+};
+
+// word w with the multiples of the odd primes below 32 (other than
+// themselves) cleared; nb10 = how many of them have p^2 <= limit
+__device__ __forceinline__ uint32_t small_word(const SmallTables &T, uint32_t w, uint32_t n_idx,
+                                               uint32_t nb10) {
+    const uint32_t i0 = 32 * w;
+    uint32_t v = i0 + 32 <= n_idx ? ~0u : (i0 >= n_idx ? 0u : (1u << (n_idx - i0)) - 1u);
+    if (w == 0) v &= ~1u;  // 1 is not prime
+    uint32_t mask = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < 10; ++k) {
+        if (k >= nb10) break;
+        const uint32_t p = T.p[k];
+        const uint32_t r = i0 - p * __umulhi(i0, T.magic[k]);  // i0 mod p
+        const uint32_t hp = (p - 1) / 2;  // p | 2i + 1  <=>  i = hp mod p
+        const uint32_t y = hp >= r ? hp - r : hp + p - r;  // first such i >= i0, minus i0
+        mask |= T.rep[k] << y;
+    }
+    if (w == 0) mask &= ~0xcb6eu;  // bits (p-1)/2 of the primes 3..31 themselves
+    return v & ~mask;
+}
+
+__global__ void __launch_bounds__(kSmallThreads) prime_small_kernel(uint64_t limit,
                                                                      uint32_t *__restrict__ out,
                                                                      PrimeInfo *__restrict__ info) {
-    extern __shared__ uint8_t flag[];  // flag[i] for the odd number 2i+1
-    __shared__ uint32_t base[128];
-    __shared__ uint32_t nbase;
-    const uint32_t r = (uint32_t)isqrt_u64(limit);  // <= 362
-    const uint32_t n_idx = (uint32_t)((limit + 1) / 2);  // odd numbers <= limit
-    if (threadIdx.x < 32) {
-        // odd base primes <= r by trial division, ordered by a warp ballot
-        uint32_t nb = 0;
-        for (uint32_t c0 = 3; c0 <= r; c0 += 64) {
-            const uint32_t cand = c0 + 2 * threadIdx.x;
-            bool prime = cand <= r;
-            for (uint32_t d = 3; prime && d * d <= cand; d += 2) prime = cand % d != 0;
-            const uint32_t bal = __ballot_sync(0xffffffffu, prime);
-            if (prime) base[nb + __popc(bal & ((1u << threadIdx.x) - 1u))] = cand;
-            nb += __popc(bal);
+    extern __shared__ uint32_t stage[];  // kSmallStage primes
+    // the constant tables go to shared memory in one parallel round trip (a
+    // cold constant cache would serialise one miss per line inside the loop)
+    __shared__ SmallTables T;
+    __shared__ uint32_t s_nb;
+    if (threadIdx.x < kNumOddBase) {
+        const uint32_t p = c_odd_base[threadIdx.x];
+        T.p[threadIdx.x] = p;
+        T.magic[threadIdx.x] = c_odd_magic[threadIdx.x];
+        if (threadIdx.x < 10) T.rep[threadIdx.x] = c_odd_rep[threadIdx.x];
+        // odd base primes with p^2 <= limit: the last one records the count
+        const bool in = (uint64_t)p * p <= limit;
+        const bool next_in = threadIdx.x + 1 < kNumOddBase &&
+                             (uint64_t)c_odd_base[threadIdx.x + 1] * c_odd_base[threadIdx.x + 1] <= limit;
+        if (threadIdx.x == 0 && !in) s_nb = 0;
+        if (in && !next_in) s_nb = threadIdx.x + 1;
+    }
+    __syncthreads();
+    const uint32_t nb = s_nb;
+    const uint32_t n_idx = (uint32_t)((limit + 1) / 2);  // odd numbers <= limit (index i: 2i+1)
+    const uint32_t n_words = (n_idx + 31) / 32;
+    const uint32_t wpt = n_words <= kSmallThreads ? 1 : 2;
+    const uint32_t w0 = wpt * threadIdx.x;
+    __shared__ __align__(8) uint32_t bits[2 * kSmallThreads];
+    bits[w0] = small_word(T, w0, n_idx, min(nb, 10u));
+    if (wpt == 2) bits[w0 + 1] = small_word(T, w0 + 1, n_idx, min(nb, 10u));
+    __syncthreads();
+    if (nb > 10) {  // p >= 37: clear p^2, p^2 + 2p, ... ; nl threads per prime
+        const uint32_t np = nb - 10, nl = kSmallThreads / np;
+        const uint32_t g = threadIdx.x % np, l = threadIdx.x / np;
+        if (l < nl) {
+            const uint32_t p = T.p[10 + g];
+            for (uint32_t i = (p * p - 1) / 2 + l * p; i < n_idx; i += nl * p)
+                atomicAnd(&bits[i >> 5], ~(1u << (i & 31)));
         }
-        if (threadIdx.x == 0) nbase = nb;
+        __syncthreads();
     }
-    for (uint32_t i = threadIdx.x; i < n_idx; i += blockDim.x) flag[i] = i != 0;  // 1 is not prime
-    __syncthreads();
-    for (uint32_t k = 0; k < nbase; ++k) {
-        const uint32_t p = base[k];
-        for (uint32_t i = (p * p - 1) / 2 + threadIdx.x * p; i < n_idx; i += blockDim.x * p)
-            flag[i] = 0;
-    }
-    __syncthreads();
-    const uint32_t chunk = (n_idx + blockDim.x - 1) / blockDim.x;
-    const uint32_t lo = min(threadIdx.x * chunk, n_idx), hi = min(lo + chunk, n_idx);
-    uint32_t cnt = 0;
-    for (uint32_t i = lo; i < hi; ++i) cnt += flag[i];
-    using Scan = cub::BlockScan<uint32_t, kSieveThreads>;
+    const uint32_t v0 = bits[w0];
+    const uint32_t v1 = wpt == 2 ? bits[w0 + 1] : 0u;
+    using Scan = cub::BlockScan<uint32_t, kSmallThreads>;
     __shared__ typename Scan::TempStorage tmp;
     uint32_t off, total;
-    Scan(tmp).ExclusiveSum(cnt, off, total);
-    uint32_t pos = off + (limit >= 2 ? 1 : 0);
-    for (uint32_t i = lo; i < hi; ++i)
-        if (flag[i]) out[pos++] = 2 * i + 1;
+    Scan(tmp).ExclusiveSum((uint32_t)(__popc(v0) + __popc(v1)), off, total);
+    for (uint32_t x = v0; x; x &= x - 1) stage[off++] = 2 * (32 * w0 + __ffs(x) - 1) + 1;
+    for (uint32_t x = v1; x; x &= x - 1) stage[off++] = 2 * (32 * w0 + 32 + __ffs(x) - 1) + 1;
+    __syncthreads();
+    const uint32_t two = limit >= 2 ? 1 : 0;
+    for (uint32_t i = threadIdx.x; i < total; i += kSmallThreads) out[two + i] = stage[i];
     if (threadIdx.x == 0) {
-        if (limit >= 2) out[0] = 2;
-        fill_info(info, total + (limit >= 2 ? 1 : 0));
+        if (two) out[0] = 2;
+        fill_info(info, total + two);
     }
 }
 
@@ -234,14 +306,16 @@ void generate_primes_async(uint64_t limit) {
     const uint64_t nseg = ceil_div(n_odd, kSegOdds);
     if (nseg == 1) {  // small tables: one CTA does everything
         c.primes_u32.reserve(pi_upper(limit) * 4);
+        static_assert(kSegWords <= 2 * kSmallThreads, "prime_small_kernel: <= 2 words per thread");
         static bool attr = false;
         if (!attr) {
             SQF2K_CUDA(cudaFuncSetAttribute(prime_small_kernel,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSegOdds));
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            kSmallStage * 4));
             attr = true;
         }
-        launch("primes_small", prime_small_kernel, dim3(1), dim3(kSieveThreads),
-               (size_t)std::max<uint64_t>(n_odd, 16), limit, c.primes_u32.as<uint32_t>(), info);
+        launch("primes_small", prime_small_kernel, dim3(1), dim3(kSmallThreads),
+               (size_t)kSmallStage * 4, limit, c.primes_u32.as<uint32_t>(), info);
         return;
     }
 

@@ -119,6 +119,7 @@ constexpr int kRingWords = 4 * kTileWords;  // power of two
 struct TileSmem {
     uint32_t ring[kRingWords];
     unsigned long long first[kDepthMax + 1];
+    uint32_t first_t[6];          // k <= 5: least tile-local slot in the last tracked tile
     uint32_t cnt[kDepthMax + 1];  // counts of k >= 6 (rare)
     uint32_t need;
     // words left after the main passes of tile t (queue t & 1), finished
@@ -278,13 +279,17 @@ __device__ __forceinline__ void scan_residue(TileSmem &S, const TileParams &P, u
 
 // One pass of the main scan on one word; k = 1 is not counted (hist[1] is
 // derived from the scanned-slot count by conservation, see verify.cu).
+// TRACK: the warp's least slot with exponent k (one REDUX, one 32-bit atomic
+// per warp; all lanes execute the scan together).
 template <bool TRACK, bool COUNT>
 __device__ __forceinline__ void pass(uint32_t &pend, uint32_t sl, uint32_t &cnt, int k,
-                                     uint32_t need, uint64_t u0, TileSmem &S) {
+                                     uint32_t need, uint32_t wl, TileSmem &S) {
     const uint32_t nw = pend & sl;
     if (COUNT) cnt += __popc(nw);
-    if (TRACK && nw && ((need >> k) & 1u))
-        atomicMin(&S.first[k], (unsigned long long)(u0 + __ffs(nw) - 1));
+    if (TRACK && ((need >> k) & 1u)) {
+        const uint32_t m = __reduce_min_sync(0xffffffffu, nw ? 32 * wl + __ffs(nw) - 1 : ~0u);
+        if (m != ~0u && (threadIdx.x & 31) == 0) atomicMin(&S.first_t[k], m);
+    }
     pend &= ~sl;
 }
 
@@ -293,13 +298,13 @@ __device__ __forceinline__ void pass(uint32_t &pend, uint32_t sl, uint32_t &cnt,
 // passes.
 template <bool TRACK, int KMAIN>
 __device__ __forceinline__ uint32_t scan_word(uint32_t pend, uint32_t prv, uint32_t cur,
-                                              uint32_t (&c)[6], uint32_t need, uint64_t u0,
+                                              uint32_t (&c)[6], uint32_t need, uint32_t wl,
                                               TileSmem &S) {
-    pass<TRACK, false>(pend, __funnelshift_l(prv, cur, 1), c[1], 1, need, u0, S);
-    if (KMAIN >= 2) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 2), c[2], 2, need, u0, S);
-    if (KMAIN >= 3) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 4), c[3], 3, need, u0, S);
-    if (KMAIN >= 4) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 8), c[4], 4, need, u0, S);
-    if (KMAIN >= 5) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 16), c[5], 5, need, u0, S);
+    pass<TRACK, false>(pend, __funnelshift_l(prv, cur, 1), c[1], 1, need, wl, S);
+    if (KMAIN >= 2) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 2), c[2], 2, need, wl, S);
+    if (KMAIN >= 3) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 4), c[3], 3, need, wl, S);
+    if (KMAIN >= 4) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 8), c[4], 4, need, wl, S);
+    if (KMAIN >= 5) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 16), c[5], 5, need, wl, S);
     return pend;
 }
 
@@ -340,7 +345,7 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
             }
             scanned += __popc(pend);
         }
-        left[i] = scan_word<TRACK, KMAIN>(pend, prv[i], cur[i], c, need, u0, S);
+        left[i] = scan_word<TRACK, KMAIN>(pend, prv[i], cur[i], c, need, w0 + i, S);
         any |= left[i];
     }
     if (!EDGE) scanned += 32 * W;
@@ -415,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         S.first[threadIdx.x] = ~0ull;
         S.cnt[threadIdx.x] = 0;
     }
+    if (threadIdx.x < 6) S.first_t[threadIdx.x] = ~0u;
     if (threadIdx.x < 2) S.n_res[threadIdx.x] = 0;
     if (threadIdx.x == 0) S.need = ~0u;
     uint32_t pbase = (uint32_t)((b0 / 32) % kPatWords);
@@ -452,9 +458,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         // ---- X(t): clear the odd multiples of p^2, p >= 11 ----
         // S.first[k] keeps this CTA's least slot with exponent k (slots grow
         // with t and residue words finish in tile order); stop tracking a k
-        // once it is known.  S.first is never reset.
-        if (FUSED && threadIdx.x >= 1 && threadIdx.x <= kDepthMax && S.first[threadIdx.x] != ~0ull)
-            atomicAnd(&S.need, ~(1u << threadIdx.x));
+        // once it is known.  S.first is never reset.  k <= 5 come from the
+        // scan's per-tile minima of tile t - 1, k >= 6 from residue words.
+        if (FUSED && threadIdx.x >= 1 && threadIdx.x <= kDepthMax) {
+            if (threadIdx.x <= 5 && S.first_t[threadIdx.x] != ~0u) {
+                const unsigned long long f = tb - kTile + S.first_t[threadIdx.x];
+                if (f < S.first[threadIdx.x]) S.first[threadIdx.x] = f;
+                S.first_t[threadIdx.x] = ~0u;
+            }
+            if (S.first[threadIdx.x] != ~0ull) atomicAnd(&S.need, ~(1u << threadIdx.x));
+        }
         if (FUSED && threadIdx.x == 0) S.n_res[t & 1u] = 0;  // tile t - 2's queue is done
 #ifndef SQF2K_EXP_NO_SCATTER
         scatter_medium(L, ring_addr + 4 * hb, kTile);
@@ -490,8 +503,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         __syncthreads();
     }
 
-    if (FUSED) {  // the last tile's deferred words, then this CTA's minima
+    if (FUSED) {  // the last tile's deferred words and minima, then this CTA's
         if (KMAIN == 5) drain_residue(S, P, t1 - 1, S.need);
+        if (threadIdx.x >= 1 && threadIdx.x <= 5 && S.first_t[threadIdx.x] != ~0u) {
+            const unsigned long long f = (uint64_t)(t1 - 1) * kTile + S.first_t[threadIdx.x];
+            if (f < S.first[threadIdx.x]) S.first[threadIdx.x] = f;
+        }
         __syncthreads();
         if (threadIdx.x >= 1 && threadIdx.x <= kDepthMax) {
             const unsigned long long f = S.first[threadIdx.x];

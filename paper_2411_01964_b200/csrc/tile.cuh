@@ -59,13 +59,10 @@ constexpr uint32_t kPiSubRoot = 1028;   // pi(8191): last "dense" bucket prime (
 constexpr int kClasses = 22;  // up to p < 2^32
 // pi(2^m) for m = 10..32 (OEIS A007053): class boundaries of a table that
 // holds every prime <= limit.
-__host__ __device__ inline uint32_t pi_pow2(int j) {
-    const uint32_t t[kClasses + 1] = {
-        172u,      309u,      564u,      1028u,     1900u,      3512u,      6542u,     12251u,
-        23000u,    43390u,    82025u,    155611u,   295947u,    564163u,    1077871u,  2063689u,
-        3957809u,  7603553u,  14630843u, 28192750u, 54400028u, 105097565u, 203280221u};
-    return t[j];
-}
+#define SQF2K_PI_POW2                                                                       \
+    {172u,      309u,      564u,      1028u,     1900u,      3512u,      6542u,     12251u,  \
+     23000u,    43390u,    82025u,    155611u,   295947u,    564163u,    1077871u,  2063689u, \
+     3957809u,  7603553u,  14630843u, 28192750u, 54400028u, 105097565u, 203280221u}
 
 // Prime-table split, kept in device memory so no host sync is needed.
 struct PrimeInfo {
