@@ -210,38 +210,42 @@ __device__ __forceinline__ void scatter_bucket(uint32_t wbase, const TileParams 
 
 // Start WORDS words (domain slot `base`, ring word `at`, 16-byte aligned and
 // not wrapping) from the p = 3, 5, 7 pattern; pbase is (base / 32) mod
-// kPatWords.  Thread i writes words 4i..4i+3 with one STS.128.  EDGE
-// applies the n < 1 zero region and the domain end.
+// kPatWords.  Thread i writes the 4-word chunks i, i + kThreads, ... with
+// one STS.128 each.  EDGE applies the n < 1 zero region and the domain end.
 template <int WORDS, bool EDGE>
 __device__ __forceinline__ void init_words(uint32_t *ring, uint32_t at, uint64_t base,
                                            uint32_t pbase, const TileParams &P) {
-    static_assert(WORDS % 4 == 0 && WORDS <= 4 * kThreads, "one uint4 per thread");
-    const uint32_t w = 4 * threadIdx.x;
-    if (WORDS < 4 * kThreads && w >= (uint32_t)WORDS) return;
-    const uint32_t *src = P.pattern + pbase + w;  // padded table: no wrap
-    uint32_t v[4];
+    static_assert(WORDS % 4 == 0, "whole uint4 chunks");
 #pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = __ldg(src + i);
-    if (EDGE) {
+    for (int c = 0; c < (WORDS + 4 * kThreads - 1) / (4 * kThreads); ++c) {
+        const uint32_t w = 4 * (threadIdx.x + c * kThreads);
+        if (WORDS % (4 * kThreads) != 0 && w >= (uint32_t)WORDS) break;
+        const uint32_t *src = P.pattern + pbase + w;  // padded table: no wrap
+        uint32_t v[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint64_t u0 = base + 32ull * (w + i);
-            if (u0 < P.z) v[i] = (u0 + 32 <= P.z) ? 0u : (v[i] & (~0u << (uint32_t)(P.z - u0)));
-            if (u0 + 32 > P.U) v[i] = (u0 >= P.U) ? 0u : (v[i] & ((1u << (uint32_t)(P.U - u0)) - 1u));
+        for (int i = 0; i < 4; ++i) v[i] = __ldg(src + i);
+        if (EDGE) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint64_t u0 = base + 32ull * (w + i);
+                if (u0 < P.z) v[i] = (u0 + 32 <= P.z) ? 0u : (v[i] & (~0u << (uint32_t)(P.z - u0)));
+                if (u0 + 32 > P.U) v[i] = (u0 >= P.U) ? 0u : (v[i] & ((1u << (uint32_t)(P.U - u0)) - 1u));
+            }
         }
+        *reinterpret_cast<uint4 *>(&ring[at + w]) = make_uint4(v[0], v[1], v[2], v[3]);
     }
-    *reinterpret_cast<uint4 *>(&ring[at + w]) = make_uint4(v[0], v[1], v[2], v[3]);
 }
 
-// The pre-tile starts the H = HW*32 halo slots (HW in {32, 64, ..., kTileWords}).
+// The pre-tile starts the H = HW*32 halo slots (HW in {32, 64, ..., 1024}).
 __device__ __forceinline__ void init_halo(uint32_t *ring, uint32_t at, uint32_t HW, uint64_t base,
                                           uint32_t pbase, const TileParams &P) {
-    if (HW == kTileWords) init_words<kTileWords, true>(ring, at, base, pbase, P);
-    else if (HW == kTileWords / 2) init_words<kTileWords / 2, true>(ring, at, base, pbase, P);
-    else if (HW == kTileWords / 4) init_words<kTileWords / 4, true>(ring, at, base, pbase, P);
-    else if (HW == kTileWords / 8) init_words<kTileWords / 8, true>(ring, at, base, pbase, P);
-    else if (HW == kTileWords / 16) init_words<kTileWords / 16, true>(ring, at, base, pbase, P);
-    else init_words<kTileWords / 32, true>(ring, at, base, pbase, P);
+    static_assert(kHaloWordsMax <= 1024 && kHaloWordsMax <= kTileWords, "halo within a quarter");
+    if (HW == 1024) init_words<1024, true>(ring, at, base, pbase, P);
+    else if (HW == 512) init_words<512, true>(ring, at, base, pbase, P);
+    else if (HW == 256) init_words<256, true>(ring, at, base, pbase, P);
+    else if (HW == 128) init_words<128, true>(ring, at, base, pbase, P);
+    else if (HW == 64) init_words<64, true>(ring, at, base, pbase, P);
+    else init_words<32, true>(ring, at, base, pbase, P);
 }
 
 __device__ __forceinline__ void append(unsigned long long *list, unsigned long long *count,
@@ -308,64 +312,63 @@ __device__ __forceinline__ uint32_t scan_word(uint32_t pend, uint32_t prv, uint3
     return pend;
 }
 
-// Exponent passes over the tile (ring quarter at hb): thread t owns the four
-// consecutive words 4t..4t+3 (one LDS.128 plus the left neighbour).  EDGE
-// masks the scan range, TRACK records per-k least slots while this CTA
-// still lacks them.  Words left after KMAIN passes (~0.02% for KMAIN = 5)
-// are queued for the next start phase.
+// Exponent passes over the tile (ring quarter at hb): thread t owns the
+// kWordsPerThread consecutive words from W*t, taken 4 at a time (one LDS.128
+// plus the left neighbour).  EDGE masks the scan range, TRACK records per-k
+// least slots while this CTA still lacks them.  Words left after KMAIN passes
+// (~0.02% for KMAIN = 5) are queued for the next tile's scan phase.
 template <bool EDGE, bool TRACK, int KMAIN>
 __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint32_t hb,
                                           uint64_t tb, uint32_t need, uint32_t (&c)[6],
                                           uint32_t &scanned, uint32_t qi) {
     constexpr int W = kWordsPerThread;
-    const uint32_t w0 = W * threadIdx.x;
-    uint32_t cur[W], prv[W];
-    if (W == 4) {
+    static_assert(W % 4 == 0, "4-word chunks");
+    const uint32_t wt = W * threadIdx.x;
+    uint32_t prv_in = S.ring[(hb + wt - 1) & (kRingWords - 1)];
+#pragma unroll
+    for (int ch = 0; ch < W / 4; ++ch) {
+        const uint32_t w0 = wt + 4 * ch;
         const uint4 cw = *reinterpret_cast<const uint4 *>(&S.ring[hb + w0]);
-        cur[0] = cw.x; cur[1 % W] = cw.y; cur[2 % W] = cw.z; cur[3 % W] = cw.w;
-    } else {
-        const uint2 cw = *reinterpret_cast<const uint2 *>(&S.ring[hb + w0]);
-        cur[0] = cw.x; cur[1 % W] = cw.y;
-    }
-    prv[0] = S.ring[(hb + w0 - 1) & (kRingWords - 1)];
+        const uint32_t cur[4] = {cw.x, cw.y, cw.z, cw.w};
+        const uint32_t prv[4] = {prv_in, cw.x, cw.y, cw.z};
+        prv_in = cw.w;
+        uint32_t left[4], any = 0;
 #pragma unroll
-    for (int i = 1; i < W; ++i) prv[i] = cur[i - 1];
-    uint32_t left[W], any = 0;
-#pragma unroll
-    for (int i = 0; i < W; ++i) {
-        const uint64_t u0 = tb + 32ull * (w0 + i);
-        uint32_t pend = ~0u;
-        if (EDGE) {
-            if (u0 + 32 <= P.scan_lo || u0 >= P.U) {
-                pend = 0u;
-            } else {
-                if (u0 < P.scan_lo) pend &= ~0u << (uint32_t)(P.scan_lo - u0);
-                if (u0 + 32 > P.U) pend &= (1u << (uint32_t)(P.U - u0)) - 1u;
-                if (P.one_u >= u0 && P.one_u < u0 + 32) pend &= ~(1u << (uint32_t)(P.one_u - u0));
-            }
-            scanned += __popc(pend);
-        }
-        left[i] = scan_word<TRACK, KMAIN>(pend, prv[i], cur[i], c, need, w0 + i, S);
-        any |= left[i];
-    }
-    if (!EDGE) scanned += 32 * W;
-    if (any) {
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-            if (!left[i]) continue;
+        for (int i = 0; i < 4; ++i) {
             const uint64_t u0 = tb + 32ull * (w0 + i);
-            if (KMAIN == 5) {
-                const uint32_t e = atomicAdd(&S.n_res[qi], 1u);
-                if (e < (uint32_t)kResCap) {  // deferred to the next tile's scan phase
-                    S.res_w[qi][e] = w0 + i;
-                    S.res_p[qi][e] = left[i];
+            uint32_t pend = ~0u;
+            if (EDGE) {
+                if (u0 + 32 <= P.scan_lo || u0 >= P.U) {
+                    pend = 0u;
                 } else {
-                    scan_residue(S, P, hb, w0 + i, u0, left[i], need);
+                    if (u0 < P.scan_lo) pend &= ~0u << (uint32_t)(P.scan_lo - u0);
+                    if (u0 + 32 > P.U) pend &= (1u << (uint32_t)(P.U - u0)) - 1u;
+                    if (P.one_u >= u0 && P.one_u < u0 + 32) pend &= ~(1u << (uint32_t)(P.one_u - u0));
                 }
-            } else if (P.k_max > P.k_eff) {  // k_eff = KMAIN < 5: leftovers leave the tile
-                spill_word(left[i], u0, P.base_n, P.esc, P.esc_count, P.esc_cap);
-            } else {
-                spill_word(left[i], u0, P.base_n, P.fail, P.fail_count, P.fail_cap);
+                scanned += __popc(pend);
+            }
+            left[i] = scan_word<TRACK, KMAIN>(pend, prv[i], cur[i], c, need, w0 + i, S);
+            any |= left[i];
+        }
+        if (!EDGE) scanned += 128;
+        if (any) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (!left[i]) continue;
+                const uint64_t u0 = tb + 32ull * (w0 + i);
+                if (KMAIN == 5) {
+                    const uint32_t e = atomicAdd(&S.n_res[qi], 1u);
+                    if (e < (uint32_t)kResCap) {  // deferred to the next tile's scan phase
+                        S.res_w[qi][e] = w0 + i;
+                        S.res_p[qi][e] = left[i];
+                    } else {
+                        scan_residue(S, P, hb, w0 + i, u0, left[i], need);
+                    }
+                } else if (P.k_max > P.k_eff) {  // k_eff = KMAIN < 5: leftovers leave the tile
+                    spill_word(left[i], u0, P.base_n, P.esc, P.esc_count, P.esc_cap);
+                } else {
+                    spill_word(left[i], u0, P.base_n, P.fail, P.fail_count, P.fail_cap);
+                }
             }
         }
     }
@@ -393,7 +396,8 @@ __device__ __forceinline__ void drain_residue(TileSmem &S, const TileParams &P, 
 //         quarter (t + 1) & 3 -- nothing in Y(t) reads that quarter.
 template <bool FUSED, int KMAIN>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TileParams P) {
-    static_assert(kWordsPerThread == 4, "init_words and scan_tile own 4 words per thread");
+    static_assert(kWordsPerThread % 4 == 0 && kThreads * kWordsPerThread == kTileWords,
+                  "4-word chunks per thread");
     static_assert(kThreads / 32 == 8, "drain_residue rotates over 8 warps");
     extern __shared__ __align__(16) uint8_t smem_raw[];
     TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
@@ -478,8 +482,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         const bool more = t + 1 < t1;
         const bool edge1 = t + 1 < ti0 || t + 1 >= ti1;
         if (!FUSED) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(&S.ring[hb + 4 * threadIdx.x]);
-            *reinterpret_cast<uint4 *>(&P.bits_out[(uint64_t)t * kTileWords + 4 * threadIdx.x]) = v;
+#pragma unroll
+            for (int ch = 0; ch < kWordsPerThread / 4; ++ch) {
+                const uint32_t w = 4 * (threadIdx.x + ch * kThreads);
+                const uint4 v = *reinterpret_cast<const uint4 *>(&S.ring[hb + w]);
+                *reinterpret_cast<uint4 *>(&P.bits_out[(uint64_t)t * kTileWords + w]) = v;
+            }
         } else {
             const uint32_t need = S.need;
 #ifndef SQF2K_EXP_NO_SCAN
@@ -531,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
 // -------------------------------------------------------------------------
 // Medium-prime scatter schedule, built on the host from the table's primes in
 // [11, kPMed) and cached on the device per set.  A prime with h = kTile/q
-// hits per tile (q = p^2) and h >= 16 is swept by whole warps (S sweeps of
+// hits per tile (q = p^2) and h >= 16*item is swept by whole warps (S sweeps of
 // ~item hits per lane: lane l starts at hit l + 32s, step 32*S*q); a rarer
 // prime is split into ~item-hit descriptors (start j, step parts*q).
 // Descriptors sorted by trip count fill 32-lane tasks, and the tasks go to
@@ -549,7 +557,7 @@ MedTables build_med(const std::vector<uint32_t> &med_primes) {
         double trips;
         uint32_t x, y;
     };
-    for (double item = kItemHits;; item *= 1.5) {
+    for (double item = kItemHits; item <= kTile; item *= 1.5) {
         MedTables t;
         std::vector<Desc> descs;
         for (uint32_t p : med_primes) {
@@ -557,7 +565,7 @@ MedTables build_med(const std::vector<uint32_t> &med_primes) {
             const uint32_t q = p * p, m = (uint32_t)t.q.size();
             t.q.push_back(q);
             const double h = (double)kTile / q;
-            if (h >= 16.0) {
+            if (h >= 16.0 * item) {  // >= item/2 hits per lane
                 const uint32_t S = std::max<uint32_t>(1, (uint32_t)(h / (32.0 * item) + 0.5));
                 for (uint32_t sw = 0; sw < S; ++sw)
                     for (uint32_t l = 0; l < 32; ++l)
@@ -592,6 +600,7 @@ MedTables build_med(const std::vector<uint32_t> &med_primes) {
         t.n_tasks = n_tasks;
         return t;
     }
+    throw Error{SQF2K_ECUDA, "medium-prime schedule does not fit the task slots"};
 }
 
 struct MedCache {

@@ -26,18 +26,18 @@
 namespace sqf2k {
 
 #ifndef SQF2K_TILE_SHIFT
-#define SQF2K_TILE_SHIFT 15
+#define SQF2K_TILE_SHIFT 16
 #endif
 constexpr int kTileShift = SQF2K_TILE_SHIFT;
-constexpr int kTile = 1 << kTileShift;  // slots per tile (32768)
-constexpr int kTileWords = kTile / 32;  // 1024 packed words
+constexpr int kTile = 1 << kTileShift;  // slots per tile (65536)
+constexpr int kTileWords = kTile / 32;  // 2048 packed words
 #ifndef SQF2K_WORDS_PER_THREAD
-#define SQF2K_WORDS_PER_THREAD 4
+#define SQF2K_WORDS_PER_THREAD 8
 #endif
 constexpr int kWordsPerThread = SQF2K_WORDS_PER_THREAD;  // words per thread in pack and scan
 constexpr int kThreads = kTileWords / kWordsPerThread;  // CTA size
 #ifndef SQF2K_CTAS_PER_SM
-#define SQF2K_CTAS_PER_SM 6
+#define SQF2K_CTAS_PER_SM 4
 #endif
 constexpr int kCtasPerSm = SQF2K_CTAS_PER_SM;
 constexpr int kDepthMax = 16;           // max exponent resolved in-tile
@@ -45,7 +45,10 @@ constexpr int kHaloMax = 1 << (kDepthMax - 1);
 constexpr int kHaloWordsMax = kHaloMax / 32;
 constexpr uint32_t kPMed = 1024;        // medium primes: 11 <= p < kPMed
 constexpr int kMaxMed = 176;            // pi(1023) - 4 = 168
-constexpr int kTaskSlots = 4;           // 32-lane scatter tasks per warp (registers)
+#ifndef SQF2K_TASK_SLOTS
+#define SQF2K_TASK_SLOTS 2
+#endif
+constexpr int kTaskSlots = SQF2K_TASK_SLOTS;  // 32-lane scatter tasks per warp (registers)
 constexpr int kItemHits = 4;            // target hits per lane per tile
 constexpr uint32_t kPatWords = 9 * 25 * 49;  // period of the p = 3, 5, 7 pattern in words
 constexpr int kResCap = 256;           // deferred residue words per tile

@@ -340,7 +340,7 @@ def test_single_cta_long_runs(monkeypatch, depth):
     # (regression: a missing barrier let it drain stale shared memory)
     monkeypatch.setenv("SQF2K_DEBUG_GRID", "1")
     for lo, tiles in [(1, 13), ((1 << 33) + 1, 11), ((1 << 46) + 12345, 9)]:
-        hi = lo + 2 * tiles * 32768 + 2 * 777
+        hi = lo + 2 * tiles * 65536 + 2 * 777
         want = O.verify(lo, hi, width=1 << 30, k_max=30)
         for _ in range(2):
             got = verify_range(lo, hi, 30, tile_depth=depth)
