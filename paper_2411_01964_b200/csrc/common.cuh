@@ -64,6 +64,10 @@ struct Context {
     int sm_count = 0;
     size_t smem_optin = 0;
     cudaStream_t stream = nullptr;
+    // side stream for work independent of the prime table (fork/join by events,
+    // captured into the same graph as parallel branches)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::recursive_mutex mu;
 
     // profiling: events recorded around launches, resolved lazily
@@ -94,23 +98,42 @@ struct Context {
 Context &ctx();            // throws Error{SQF2K_ENODEV} if not initialised
 Context *ctx_or_null();
 
-// Launch `kernel` on the library stream, bracketed by events when profiling.
+// Launch `kernel` on stream `st`, bracketed by events when profiling.
 template <class Kernel, class... Args>
-void launch(const char *name, Kernel kernel, dim3 grid, dim3 block, size_t smem,
-            Args... args) {
+void launch_on(cudaStream_t st, const char *name, Kernel kernel, dim3 grid, dim3 block,
+               size_t smem, Args... args) {
     Context &c = ctx();
     cudaEvent_t a = nullptr, b = nullptr;
     if (c.profiling) {
         a = c.get_event();
         b = c.get_event();
-        SQF2K_CUDA(cudaEventRecord(a, c.stream));
+        SQF2K_CUDA(cudaEventRecord(a, st));
     }
-    kernel<<<grid, block, smem, c.stream>>>(args...);
+    kernel<<<grid, block, smem, st>>>(args...);
     SQF2K_CUDA(cudaGetLastError());
     if (c.profiling) {
-        SQF2K_CUDA(cudaEventRecord(b, c.stream));
+        SQF2K_CUDA(cudaEventRecord(b, st));
         c.pending.push_back({c.stat_index(name), a, b});
     }
+}
+
+// Launch `kernel` on the library stream.
+template <class Kernel, class... Args>
+void launch(const char *name, Kernel kernel, dim3 grid, dim3 block, size_t smem,
+            Args... args) {
+    launch_on(ctx().stream, name, kernel, grid, block, smem, args...);
+}
+
+// Fork the side stream off the library stream / join it back.
+inline void fork_side() {
+    Context &c = ctx();
+    SQF2K_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+    SQF2K_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+}
+inline void join_side() {
+    Context &c = ctx();
+    SQF2K_CUDA(cudaEventRecord(c.ev_join, c.side));
+    SQF2K_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
 }
 
 // Counted host<->device copies on the library stream.

@@ -150,6 +150,13 @@ int sqf2k_init(int device) {
         delete c;
         return fail(SQF2K_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
     }
+    if ((e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming)) != cudaSuccess) {
+        cudaStreamDestroy(c->stream);
+        delete c;
+        return fail(SQF2K_ECUDA, "side stream: %s", cudaGetErrorString(e));
+    }
     if ((e = cudaMallocHost(&c->pinned, 1 << 16)) != cudaSuccess) {
         cudaStreamDestroy(c->stream);
         delete c;
@@ -177,6 +184,10 @@ void sqf2k_shutdown(void) {
         cudaEventDestroy(p.b);
     }
     for (auto e : c->event_pool) cudaEventDestroy(e);
+    cudaStreamSynchronize(c->side);
+    cudaEventDestroy(c->ev_fork);
+    cudaEventDestroy(c->ev_join);
+    cudaStreamDestroy(c->side);
     cudaStreamDestroy(c->stream);
     delete c;
     g_ctx = nullptr;

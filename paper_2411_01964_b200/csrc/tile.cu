@@ -9,6 +9,7 @@
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "finish.cuh"
 #include "tile.cuh"
 
 namespace sqf2k {
@@ -126,6 +127,7 @@ struct TileSmem {
     // while tile t + 1 is scanned
     uint32_t res_w[2][kResCap], res_p[2][kResCap];
     uint32_t n_res[2];
+    uint32_t last;  // this CTA finished last (epilogue)
 };
 
 // Clear slot o of the words starting at shared address wbase (byte address
@@ -388,6 +390,30 @@ __device__ __forceinline__ void drain_residue(TileSmem &S, const TileParams &P, 
     }
 }
 
+// Last-CTA epilogue of a single-batch call: once every CTA has added its
+// counts, the last one escalates the unresolved n (k > k_eff, exact trial
+// division, 8 warps) and copies the accumulators to mapped host memory.
+__device__ __forceinline__ void finish_call(TileSmem &S, const TileParams &P) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) S.last = atomicAdd(&P.acc->done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!S.last) return;
+    __threadfence();
+    if (P.k_max > P.k_eff) {
+        const uint64_t count = min((unsigned long long)P.esc_cap, __ldcg(P.esc_count));
+        escalate_warps(P.esc, count, P.k_eff + 1, P.k_max, P.primes, __ldcg(&P.info->count),
+                       P.hist, P.min_n, P.fail, P.fail_count, P.fail_cap, threadIdx.x / 32,
+                       kThreads / 32);
+        __threadfence();
+        __syncthreads();
+    }
+    // kernel completion makes these host writes visible to the stream's waiter
+    const unsigned long long *src = reinterpret_cast<const unsigned long long *>(P.acc);
+    unsigned long long *dst = static_cast<unsigned long long *>(P.acc_host);
+    for (uint32_t i = threadIdx.x; i < sizeof(Acc) / 8; i += kThreads) dst[i] = __ldcg(src + i);
+}
+
 // KMAIN = min(k_eff, 5) unconditional passes; the export form ignores it.
 // Per tile t, two phases between barriers:
 //   X(t): clear the medium and bucket primes' hits in quarter t & 3;
@@ -533,6 +559,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         if (lane == 0 && sc) atomicAdd(P.scanned, sc);
         if (threadIdx.x >= 6 && threadIdx.x <= kDepthMax && S.cnt[threadIdx.x])
             atomicAdd(&P.hist[threadIdx.x], (unsigned long long)S.cnt[threadIdx.x]);
+        if (P.acc) finish_call(S, P);
     }
 }
 
@@ -641,7 +668,10 @@ void launch_tile(const char *name, unsigned grid, size_t smem, const TileParams 
     launch(name, tile_kernel<FUSED, KMAIN>, dim3(grid), dim3(kThreads), smem, P);
 }
 
-void run_tile_batch(const BatchArgs &a) {
+// Work of a batch that does not need the prime table: the medium schedule
+// (host-built, cached), the p = 3, 5, 7 pattern and the bucket counters --
+// on stream `st` (the side stream for the first batch of a call).
+void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
     Context &c = ctx();
     const uint32_t n_tiles = (uint32_t)ceil_div(a.U, kTile);
 
@@ -660,13 +690,20 @@ void run_tile_batch(const BatchArgs &a) {
 
     // p = 3, 5, 7 pattern of this domain
     c.pattern.reserve((kPatWords + kTileWords) * 4);
-    launch("pattern", pattern_kernel, dim3(ceil_div(kPatWords + kTileWords, 256)), dim3(256), 0, a.base_n,
-           a.pattern_present, c.pattern.as<uint32_t>());
+    launch_on(st, "pattern", pattern_kernel, dim3(ceil_div(kPatWords + kTileWords, 256)), dim3(256),
+              0, a.base_n, a.pattern_present, c.pattern.as<uint32_t>());
+    c.tile_counts.reserve((n_tiles + 1) * 4);
+    SQF2K_CUDA(cudaMemsetAsync(c.tile_counts.ptr, 0, (n_tiles + 1) * 4, st));
+}
+
+// Bucket lists and the tile kernel of a batch (after prep_tile_batch and the
+// prime table), on the library stream.
+void run_tile_batch(const BatchArgs &a) {
+    Context &c = ctx();
+    const uint32_t n_tiles = (uint32_t)ceil_div(a.U, kTile);
 
     // bucket lists (sizes bounded on the host: no sync)
-    c.tile_counts.reserve((n_tiles + 1) * 4);
     uint32_t *counts = c.tile_counts.as<uint32_t>();
-    SQF2K_CUDA(cudaMemsetAsync(counts, 0, (n_tiles + 1) * 4, c.stream));
     const unsigned bgrid = (unsigned)c.sm_count * 8;
     const uint32_t *tile_start = nullptr;
     if (!a.exact_buckets) {
@@ -720,6 +757,10 @@ void run_tile_batch(const BatchArgs &a) {
     P.fail_cap = a.fail_cap;
     P.scanned = a.scanned;
     P.bits_out = a.bits_out;
+    P.acc = a.fused ? a.finish_acc : nullptr;
+    P.acc_host = a.finish_host;
+    P.primes = a.primes;
+    P.info = a.info;
 
     const size_t smem = tile_smem_bytes();
     uint64_t grid_cap = (uint64_t)c.sm_count * kCtasPerSm;

@@ -21,6 +21,8 @@
 
 #include <stdint.h>
 
+#include <cuda_runtime.h>
+
 #include <vector>
 
 namespace sqf2k {
@@ -102,6 +104,12 @@ struct TileParams {
     uint64_t fail_cap;
     unsigned long long *scanned; // fused mode: odd n entering the scan (hist[1] by conservation)
     uint32_t *bits_out;          // export mode: packed words of the domain
+    // last-CTA epilogue (single-batch fused calls): escalate, then copy the
+    // accumulators to mapped host memory -- no escalate launch, no memcpy
+    struct Acc *acc;             // null: no epilogue
+    void *acc_host;
+    const uint32_t *primes;
+    const PrimeInfo *info;
 };
 
 // residue of the first slot u >= 0 with q | base_n + 2u, i.e. u = -base_n/2 mod q
@@ -133,7 +141,10 @@ struct BatchArgs {
     uint32_t *bits_out;
     bool exact_buckets;           // count + scan + fill instead of fixed capacity
     unsigned int *overflow;       // set when a fixed-capacity list overflowed
+    struct Acc *finish_acc;       // non-null: the tile kernel's last CTA finishes the call
+    void *finish_host;            //   (escalation + accumulators to this mapped host buffer)
 };
+void prep_tile_batch(const BatchArgs &a, cudaStream_t st);
 void run_tile_batch(const BatchArgs &a);
 
 }  // namespace sqf2k

@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "finish.cuh"
 #include "tile.cuh"
 
 namespace sqf2k {
@@ -32,32 +33,6 @@ namespace {
 
 constexpr uint64_t kDefaultBatch = 1ull << 36;
 
-// Exact squarefree test by trial division, one warp per m (odd m >= 1):
-// lanes take the odd primes p (index >= 1) with p^2 <= m.
-__device__ bool warp_squarefree(uint64_t m, const uint32_t *__restrict__ primes,
-                                uint64_t n_primes) {
-    const int lane = threadIdx.x & 31;
-    for (uint64_t base = 1; base < n_primes; base += 32) {
-        const uint64_t i = base + lane;
-        bool live = false, hit = false;
-        if (i < n_primes) {
-            const uint64_t p = primes[i];
-            const uint64_t q = p * p;
-            live = q <= m;
-            hit = live && (m % q == 0);
-        }
-        if (__any_sync(0xffffffffu, hit)) return false;
-        if (!__any_sync(0xffffffffu, live)) break;
-    }
-    return true;
-}
-
-__device__ __forceinline__ void append(unsigned long long *list, unsigned long long *count,
-                                       uint64_t cap, uint64_t n) {
-    const unsigned long long i = atomicAdd(count, 1ull);
-    if (i < cap) list[i] = n;
-}
-
 // Escalation: n unresolved at the tile depth, exponents k_from..k_max exactly.
 __global__ void escalate_kernel(const unsigned long long *__restrict__ esc,
                                 const unsigned long long *__restrict__ esc_count, uint64_t esc_cap,
@@ -67,25 +42,9 @@ __global__ void escalate_kernel(const unsigned long long *__restrict__ esc,
                                 unsigned long long *min_n, unsigned long long *fail,
                                 unsigned long long *fail_count, uint64_t fail_cap) {
     const uint64_t count = min((unsigned long long)esc_cap, *esc_count);
-    const uint64_t n_primes = info->count;
-    const uint64_t warps = (uint64_t)gridDim.x * blockDim.x / 32;
-    for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32; i < count;
-         i += warps) {
-        const uint64_t n = esc[i];
-        uint32_t found = 0;
-        for (uint32_t k = k_from; k <= k_max && !found; ++k) {
-            if (n <= (1ull << k)) break;  // n - 2^k < 1
-            if (warp_squarefree(n - (1ull << k), primes, n_primes)) found = k;
-        }
-        if ((threadIdx.x & 31) == 0) {
-            if (found) {
-                atomicAdd(&hist[found], 1ull);
-                atomicMin(&min_n[found], (unsigned long long)n);
-            } else {
-                append(fail, fail_count, fail_cap, n);
-            }
-        }
-    }
+    escalate_warps(esc, count, k_from, k_max, primes, info->count, hist, min_n, fail, fail_count,
+                   fail_cap, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32,
+                   (uint64_t)gridDim.x * blockDim.x / 32);
 }
 
 // runner.py:105-114: least k in [1, 63] with n - 2^k squarefree, 0 if none.
@@ -128,13 +87,6 @@ __global__ void narrow_primes_kernel(const int64_t *__restrict__ in, uint32_t *_
         out[i] = (uint32_t)in[i];
 }
 
-struct Acc {
-    unsigned long long hist[SQF2K_HIST_LEN];
-    unsigned long long min_n[SQF2K_HIST_LEN];
-    unsigned long long esc_count, fail_count;
-    unsigned long long scanned;  // fused pipeline: odd n that entered the scan
-    unsigned int overflow, pad;
-};
 
 unsigned warp_grid(uint64_t items) {
     const uint64_t cap = (uint64_t)ctx().sm_count * 2;
@@ -213,61 +165,84 @@ struct VerifyPlan {
 
 void enqueue_verify(const VerifyPlan &pl) {
     Context &c = ctx();
-    generate_primes_async(pl.limit);  // prime table up to isqrt(end - 1) (runner.py:192)
     c.acc.reserve(sizeof(Acc));
     c.esc.reserve(pl.esc_cap * 8);
     c.fail.reserve(pl.dev_fail_cap * 8);
     Acc *acc = c.acc.as<Acc>();
-    SQF2K_CUDA(cudaMemsetAsync(acc, 0, sizeof(Acc), c.stream));
-    SQF2K_CUDA(cudaMemsetAsync(acc->min_n, 0xff, sizeof acc->min_n, c.stream));
     BatchArgs a;
     std::memset(&a, 0, sizeof a);
     a.k_eff = pl.k_eff;
     a.k_max = pl.k_max;
-    a.primes = c.primes_u32.as<uint32_t>();
-    a.info = c.prime_info.as<PrimeInfo>();
     a.n_primes_bound = pi_upper(pl.limit);
     a.pattern_present = pl.small.present;
     a.med_primes = &pl.small.med;
     a.hist = acc->hist;
     a.min_n = acc->min_n;
-    a.esc = c.esc.as<unsigned long long>();
     a.esc_count = &acc->esc_count;
     a.esc_cap = pl.esc_cap;
-    a.fail = c.fail.as<unsigned long long>();
     a.fail_count = &acc->fail_count;
     a.fail_cap = pl.dev_fail_cap;
     a.exact_buckets = pl.exact;
     a.overflow = &acc->overflow;
     a.scanned = &acc->scanned;
     const uint32_t H = pl.H;
-    for (uint64_t s0 = 0; s0 < pl.n_slots; s0 += pl.batch) {
+    // batch s0 covers the odd n from A = start + 2 s0 on; its domain starts H
+    // slots (the halo) below A
+    auto set_batch = [&](uint64_t s0) {
         const uint64_t sb = std::min(pl.batch, pl.n_slots - s0);
-        const uint64_t A = pl.start + 2 * s0;  // first n of the batch
+        const uint64_t A = pl.start + 2 * s0;
         a.base_n = (int64_t)A - 2 * (int64_t)H;
         a.U = H + sb;
         a.z = a.base_n < 1 ? (uint64_t)((1 - a.base_n) / 2) : 0;
-        if (pl.pipeline == 1) {
-            // two-pass: export the bitmap of [A - 2H, A + 2 sb) then scan it
-            const uint32_t nt = (uint32_t)ceil_div(a.U, kTile);
-            c.window.reserve((size_t)nt * kTile / 8 + 64);
+        if (pl.pipeline == 1) {  // two-pass: export [A - 2H, A + 2 sb), then scan it
             a.fused = false;
             a.scan_lo = 0;
             a.one_u = ~0ull;
             a.H = 0;
+            const uint32_t nt = (uint32_t)ceil_div(a.U, kTile);
+            c.window.reserve((size_t)nt * kTile / 8 + 64);
             a.bits_out = c.window.as<uint32_t>();
-            run_tile_batch(a);
-            scan_bitmap_device(c.window.as<uint32_t>(), H / 32, sb, A, pl.k_eff, pl.k_max,
-                               A == 1 ? 0 : ~0ull, acc->hist, acc->min_n, a.esc, a.esc_count,
-                               pl.esc_cap, a.fail, a.fail_count, pl.dev_fail_cap, a.scanned);
         } else {
             a.fused = true;
             a.scan_lo = H;
             a.one_u = A == 1 ? (uint64_t)H : ~0ull;
             a.H = H;
             a.bits_out = nullptr;
-            run_tile_batch(a);
         }
+        return std::make_pair(A, sb);
+    };
+    a.esc = c.esc.as<unsigned long long>();
+    a.fail = c.fail.as<unsigned long long>();
+    set_batch(0);  // allocations before the fork
+
+    // side stream: accumulators and the first batch's prime-free preparation,
+    // in parallel with the prime table (runner.py:192) on the main stream
+    fork_side();
+    SQF2K_CUDA(cudaMemsetAsync(acc, 0, sizeof(Acc), c.side));
+    SQF2K_CUDA(cudaMemsetAsync(acc->min_n, 0xff, sizeof acc->min_n, c.side));
+    prep_tile_batch(a, c.side);
+    generate_primes_async(pl.limit);
+    a.primes = c.primes_u32.as<uint32_t>();  // (re)allocated by the generator
+    a.info = c.prime_info.as<PrimeInfo>();
+    join_side();
+    // one fused batch at the default depth: the tile kernel's last CTA does
+    // the (rare) escalations and writes the accumulators to pinned memory
+    const bool finish_in_tile = pl.pipeline == 0 && pl.n_slots <= pl.batch &&
+                                pl.k_eff == (uint32_t)kDepthMax;
+    for (uint64_t s0 = 0; s0 < pl.n_slots; s0 += pl.batch) {
+        const auto [A, sb] = set_batch(s0);
+        if (s0) prep_tile_batch(a, c.stream);
+        a.finish_acc = finish_in_tile ? acc : nullptr;
+        a.finish_host = c.pinned;
+        run_tile_batch(a);
+        if (pl.pipeline == 1)
+            scan_bitmap_device(c.window.as<uint32_t>(), H / 32, sb, A, pl.k_eff, pl.k_max,
+                               A == 1 ? 0 : ~0ull, acc->hist, acc->min_n, a.esc, a.esc_count,
+                               pl.esc_cap, a.fail, a.fail_count, pl.dev_fail_cap, a.scanned);
+    }
+    if (finish_in_tile) {
+        c.d2h_bytes += sizeof(Acc);  // written to mapped host memory by the kernel
+        return;
     }
     if (pl.k_max > pl.k_eff)
         launch("escalate", escalate_kernel, dim3(warp_grid(pl.esc_cap)), dim3(256), 0,
@@ -497,6 +472,7 @@ int sieve_bits(uint64_t start, uint64_t end, const int64_t *primes_h, uint64_t n
     for (int attempt = 0; attempt < 2; ++attempt) {
         SQF2K_CUDA(cudaMemsetAsync(a.overflow, 0, sizeof(unsigned int), c.stream));
         a.exact_buckets = attempt > 0;
+        prep_tile_batch(a, c.stream);
         run_tile_batch(a);
         unsigned int &ovf = *static_cast<unsigned int *>(c.pinned);
         copy_d2h(&ovf, a.overflow, sizeof ovf);
