@@ -117,6 +117,44 @@ void launch_on(cudaStream_t st, const char *name, Kernel kernel, dim3 grid, dim3
     }
 }
 
+// Launch with programmatic dependent launch: the kernel may start while its
+// stream predecessor is still running (once that grid triggers) and must
+// execute griddepcontrol.wait before touching the predecessor's output.
+template <class... KArgs, class... Args>
+void launch_pdl(const char *name, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                Args... args) {
+    Context &c = ctx();
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (c.profiling) {  // per-launch events would serialise anyway
+        a = c.get_event();
+        b = c.get_event();
+        SQF2K_CUDA(cudaEventRecord(a, c.stream));
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = c.profiling ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SQF2K_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+    if (c.profiling) {
+        SQF2K_CUDA(cudaEventRecord(b, c.stream));
+        c.pending.push_back({c.stat_index(name), a, b});
+    }
+}
+
+// griddepcontrol (sm_90+): wait for the predecessor grid / let the dependent start
+__device__ __forceinline__ void grid_dependency_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void grid_dependents_launch() {
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
 // Launch `kernel` on the library stream.
 template <class Kernel, class... Args>
 void launch(const char *name, Kernel kernel, dim3 grid, dim3 block, size_t smem,

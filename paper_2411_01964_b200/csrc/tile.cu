@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(256) bucket_kernel(
     const uint32_t *__restrict__ primes, const PrimeInfo *__restrict__ info, int64_t base_n,
     uint64_t U, uint32_t *__restrict__ counts, const uint32_t *__restrict__ offsets,
     uint16_t *__restrict__ hits, unsigned int *__restrict__ overflow) {
+    grid_dependents_launch();  // the tile kernel may start its prime-free prologue
     __shared__ unsigned long long s_end[kClasses];  // cumulative work per class
     __shared__ uint32_t s_lo[kClasses];
     __shared__ unsigned long long s_nsub[kClasses];
@@ -463,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             init_halo(S.ring, halo_at, HW, b0, pbase, P);
             __syncthreads();
             scatter_medium(L, ring_addr + 4 * halo_at, H);
+            grid_dependency_wait();  // bucket lists from here on
             scatter_bucket(ring_addr + 4 * halo_at, P, t0 - 1, kTile - H);
             pbase += HW;
             if (pbase >= kPatWords) pbase -= kPatWords;
@@ -470,6 +472,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             for (uint32_t i = threadIdx.x; i < HW; i += kThreads) S.ring[halo_at + i] = 0u;
         }
     }
+    grid_dependency_wait();  // (no-op when already waited or not launched dependent)
     {  // tile t0's words
         const uint64_t tb = (uint64_t)t0 * kTile, hb = (t0 & 3u) * kTileWords;
         if (t0 < ti0 || t0 >= ti1) init_words<kTileWords, true>(S.ring, hb, tb, pbase, P);
@@ -665,7 +668,7 @@ void launch_tile(const char *name, unsigned grid, size_t smem, const TileParams 
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    launch(name, tile_kernel<FUSED, KMAIN>, dim3(grid), dim3(kThreads), smem, P);
+    launch_pdl(name, tile_kernel<FUSED, KMAIN>, dim3(grid), dim3(kThreads), smem, P);
 }
 
 // Work of a batch that does not need the prime table: the medium schedule
