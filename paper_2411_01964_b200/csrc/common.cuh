@@ -84,7 +84,7 @@ struct Context {
     DevBuf primes_u32, prime_bits, prime_counts, prime_offsets, scan_tmp;
     DevBuf residues, items, tile_counts, tile_offsets, hits;
     DevBuf acc, esc, fail, fail_sorted, window, kvals, bits_out, host_primes;
-    DevBuf pattern, prime_info;
+    DevBuf pattern, prime_info, sched;
     void *pinned = nullptr;  // small pinned host staging (summary readback)
     uint64_t h2d_bytes = 0, d2h_bytes = 0;  // copy accounting (bench e2e)
     uint64_t primes_limit = 0;  // primes_u32 holds all primes <= primes_limit

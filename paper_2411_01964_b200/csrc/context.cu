@@ -176,7 +176,7 @@ void sqf2k_shutdown(void) {
                       &c->scan_tmp, &c->residues, &c->items, &c->tile_counts,
                       &c->tile_offsets, &c->hits, &c->acc, &c->esc,
                       &c->fail, &c->fail_sorted, &c->window, &c->kvals, &c->bits_out,
-                      &c->host_primes, &c->pattern, &c->prime_info})
+                      &c->host_primes, &c->pattern, &c->prime_info, &c->sched})
         b->release();
     if (c->pinned) cudaFreeHost(c->pinned);
     for (auto &p : c->pending) {

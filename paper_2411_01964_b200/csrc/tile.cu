@@ -128,7 +128,8 @@ struct TileSmem {
     // while tile t + 1 is scanned
     uint32_t res_w[2][kResCap], res_p[2][kResCap];
     uint32_t n_res[2];
-    uint32_t last;  // this CTA finished last (epilogue)
+    uint32_t last;      // this CTA finished last (epilogue)
+    uint32_t chunk[2];  // the dynamic chunk just taken
 };
 
 // Clear slot o of the words starting at shared address wbase (byte address
@@ -391,16 +392,11 @@ __device__ __forceinline__ void drain_residue(TileSmem &S, const TileParams &P, 
     }
 }
 
-// Last-CTA epilogue of a single-batch call: once every CTA has added its
-// counts, the last one escalates the unresolved n (k > k_eff, exact trial
-// division, 8 warps) and copies the accumulators to mapped host memory.
+// Last-CTA epilogue of a single-batch call (run by the CTA that finished
+// last, after every CTA has added its counts): escalate the unresolved n
+// (k > k_eff, exact trial division, 8 warps) and copy the accumulators to
+// mapped host memory.
 __device__ __forceinline__ void finish_call(TileSmem &S, const TileParams &P) {
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) S.last = atomicAdd(&P.acc->done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!S.last) return;
-    __threadfence();
     if (P.k_max > P.k_eff) {
         const uint64_t count = min((unsigned long long)P.esc_cap, __ldcg(P.esc_count));
         escalate_warps(P.esc, count, P.k_eff + 1, P.k_max, P.primes, __ldcg(&P.info->count),
@@ -421,6 +417,25 @@ __device__ __forceinline__ void finish_call(TileSmem &S, const TileParams &P) {
 //   Y(t): scan tile t (fused) or store it (export), finish tile t - 1's
 //         deferred words, and start tile t + 1's words from the pattern in
 //         quarter (t + 1) & 3 -- nothing in Y(t) reads that quarter.
+// Per-CTA timeline for experiment builds (-DSQF2K_EXP_TIMELINE, tools/timeline.py).
+#ifdef SQF2K_EXP_TIMELINE
+__device__ unsigned long long g_timeline[4096][4];
+__device__ __forceinline__ void tl_mark(int i) {
+    if (threadIdx.x != 0 || blockIdx.x >= 4096) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_timeline[blockIdx.x][i] = t;
+    if (i == 3) {
+        unsigned sm;
+        asm("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_timeline[blockIdx.x][0] |= (unsigned long long)sm << 56;
+    }
+}
+#define TL(i) tl_mark(i)
+#else
+#define TL(i) do { } while (0)
+#endif
+
 template <bool FUSED, int KMAIN>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TileParams P) {
     static_assert(kWordsPerThread % 4 == 0 && kThreads * kWordsPerThread == kTileWords,
@@ -429,12 +444,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     extern __shared__ __align__(16) uint8_t smem_raw[];
     TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
     const uint32_t G = gridDim.x;
-    const uint32_t t0 = (uint32_t)((uint64_t)P.n_tiles * blockIdx.x / G);
-    const uint32_t t1 = (uint32_t)((uint64_t)P.n_tiles * (blockIdx.x + 1) / G);
-    if (t0 >= t1) return;
+    TL(0);
+    // Work: a static chunk of ~3/4 of the tiles per CTA (contiguous), then
+    // chunks handed out by a global counter -- the CTAs sharing an SM are not
+    // served evenly by the warp schedulers, and the fast ones take the rest.
+    // (short runs, < kDynMinTiles tiles per CTA, stay fully static: a chunk's
+    // start-up -- halo, offsets -- would cost more than the balance gains)
+    const bool dynamic = P.n_tiles >= (uint64_t)kDynMinTiles * G;
+    const uint32_t S1 = (uint32_t)((uint64_t)P.n_tiles * kStaticEighths / (8ull * G));
+    const uint32_t dyn0 = dynamic ? S1 * G : P.n_tiles;  // first dynamically scheduled tile
+    // dynamic chunks of ~1/(8G) of the rest: an atomicAdd each, no CAS races
+    const uint32_t csz = max((P.n_tiles - dyn0) / (8 * G), (uint32_t)kMinChunk);
+    uint32_t t0 = dynamic ? S1 * blockIdx.x : (uint32_t)((uint64_t)P.n_tiles * blockIdx.x / G);
+    uint32_t t1 = dynamic ? t0 + S1 : (uint32_t)((uint64_t)P.n_tiles * (blockIdx.x + 1) / G);
     const uint32_t H = FUSED ? P.H : 0u;
     const uint32_t HW = H / 32;
-    const bool pre = FUSED && t0 > 0;
     // tiles [ti0, ti1) need no masks: past the scan start, the n < 1 region
     // and n = 1, and wholly below the domain end
     uint64_t lo_edge = FUSED ? P.scan_lo : 0ull;
@@ -442,110 +466,136 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     if (FUSED && P.one_u != ~0ull && P.one_u + 1 > lo_edge) lo_edge = P.one_u + 1;
     const uint32_t ti0 = (uint32_t)((lo_edge + kTile - 1) / kTile);
     const uint32_t ti1 = (uint32_t)(P.U / kTile);
-
-    // medium primes: each lane's descriptors, first hits at the chunk base b0
-    const uint64_t b0 = pre ? (uint64_t)t0 * kTile - H : (uint64_t)t0 * kTile;
-    MedLane L;
-    init_medium(L, P, b0);
     if (threadIdx.x <= kDepthMax) {
         S.first[threadIdx.x] = ~0ull;
         S.cnt[threadIdx.x] = 0;
     }
     if (threadIdx.x < 6) S.first_t[threadIdx.x] = ~0u;
-    if (threadIdx.x < 2) S.n_res[threadIdx.x] = 0;
     if (threadIdx.x == 0) S.need = ~0u;
-    uint32_t pbase = (uint32_t)((b0 / 32) % kPatWords);
     const uint32_t ring_addr = smem_addr(S.ring);
-
-    // the halo just below tile t0: the tail of quarter (t0 - 1) & 3
-    const uint32_t halo_at = ((t0 + 3u) & 3u) * kTileWords + kTileWords - HW;
-    if (FUSED) {
-        if (pre) {  // pre-tile: sieve the H slots below the chunk
-            init_halo(S.ring, halo_at, HW, b0, pbase, P);
-            __syncthreads();
-            scatter_medium(L, ring_addr + 4 * halo_at, H);
-            grid_dependency_wait();  // bucket lists from here on
-            scatter_bucket(ring_addr + 4 * halo_at, P, t0 - 1, kTile - H);
-            pbase += HW;
-            if (pbase >= kPatWords) pbase -= kPatWords;
-        } else {
-            for (uint32_t i = threadIdx.x; i < HW; i += kThreads) S.ring[halo_at + i] = 0u;
-        }
-    }
-    grid_dependency_wait();  // (no-op when already waited or not launched dependent)
-    {  // tile t0's words
-        const uint64_t tb = (uint64_t)t0 * kTile, hb = (t0 & 3u) * kTileWords;
-        if (t0 < ti0 || t0 >= ti1) init_words<kTileWords, true>(S.ring, hb, tb, pbase, P);
-        else init_words<kTileWords, false>(S.ring, hb, tb, pbase, P);
-        pbase += kTileWords;
-        if (pbase >= kPatWords) pbase -= kPatWords;
-    }
-    __syncthreads();
-
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
     uint32_t scanned = 0;  // <= 128 per tile, < 2^21 tiles
-    for (uint32_t t = t0; t < t1; ++t) {
-        const uint64_t tb = (uint64_t)t * kTile;
-        const uint32_t hb = (t & 3u) * kTileWords;
-        const bool edge = t < ti0 || t >= ti1;
-        // ---- X(t): clear the odd multiples of p^2, p >= 11 ----
-        // S.first[k] keeps this CTA's least slot with exponent k (slots grow
-        // with t and residue words finish in tile order); stop tracking a k
-        // once it is known.  S.first is never reset.  k <= 5 come from the
-        // scan's per-tile minima of tile t - 1, k >= 6 from residue words.
-        if (FUSED && threadIdx.x >= 1 && threadIdx.x <= kDepthMax) {
-            if (threadIdx.x <= 5 && S.first_t[threadIdx.x] != ~0u) {
-                const unsigned long long f = tb - kTile + S.first_t[threadIdx.x];
-                if (f < S.first[threadIdx.x]) S.first[threadIdx.x] = f;
-                S.first_t[threadIdx.x] = ~0u;
+    bool waited = false;
+
+    for (;;) {
+        if (t0 >= t1) {  // next dynamic chunk: one atomic, chunk index -> tiles
+            __syncthreads();  // the last chunk's drain is done with the ring
+            if (threadIdx.x == 0) {
+                const uint32_t k = atomicAdd(&P.sched[0], 1u);
+                const uint64_t lo = (uint64_t)dyn0 + (uint64_t)k * csz;
+                S.chunk[0] = (uint32_t)min(lo, (uint64_t)P.n_tiles);
+                S.chunk[1] = (uint32_t)min(lo + csz, (uint64_t)P.n_tiles);
             }
-            if (S.first[threadIdx.x] != ~0ull) atomicAnd(&S.need, ~(1u << threadIdx.x));
+            __syncthreads();
+            t0 = S.chunk[0];
+            t1 = S.chunk[1];
+            if (t0 >= t1) break;
         }
-        if (FUSED && threadIdx.x == 0) S.n_res[t & 1u] = 0;  // tile t - 2's queue is done
-#ifndef SQF2K_EXP_NO_SCATTER
-        scatter_medium(L, ring_addr + 4 * hb, kTile);
-        scatter_bucket(ring_addr + 4 * hb, P, t, 0);
-#endif
-        __syncthreads();
-        // ---- Y(t) ----
-        const bool more = t + 1 < t1;
-        const bool edge1 = t + 1 < ti0 || t + 1 >= ti1;
-        if (!FUSED) {
-#pragma unroll
-            for (int ch = 0; ch < kWordsPerThread / 4; ++ch) {
-                const uint32_t w = 4 * (threadIdx.x + ch * kThreads);
-                const uint4 v = *reinterpret_cast<const uint4 *>(&S.ring[hb + w]);
-                *reinterpret_cast<uint4 *>(&P.bits_out[(uint64_t)t * kTileWords + w]) = v;
-            }
-        } else {
-            const uint32_t need = S.need;
-#ifndef SQF2K_EXP_NO_SCAN
-            if (need & 0x3eu) {
-                if (edge) scan_tile<true, true, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
-                else scan_tile<false, true, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+        const bool pre = FUSED && t0 > 0;
+        // medium primes: each lane's descriptors, first hits at the chunk base b0
+        const uint64_t b0 = pre ? (uint64_t)t0 * kTile - H : (uint64_t)t0 * kTile;
+        MedLane L;
+        init_medium(L, P, b0);
+        if (threadIdx.x < 2) S.n_res[threadIdx.x] = 0;
+        uint32_t pbase = (uint32_t)((b0 / 32) % kPatWords);
+
+        // the halo just below tile t0: the tail of quarter (t0 - 1) & 3
+        const uint32_t halo_at = ((t0 + 3u) & 3u) * kTileWords + kTileWords - HW;
+        if (FUSED) {
+            if (pre) {  // pre-tile: sieve the H slots below the chunk
+                init_halo(S.ring, halo_at, HW, b0, pbase, P);
+                __syncthreads();
+                scatter_medium(L, ring_addr + 4 * halo_at, H);
+                if (!waited) grid_dependency_wait();  // bucket lists from here on
+                waited = true;
+                scatter_bucket(ring_addr + 4 * halo_at, P, t0 - 1, kTile - H);
+                pbase += HW;
+                if (pbase >= kPatWords) pbase -= kPatWords;
             } else {
-                if (edge) scan_tile<true, false, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
-                else scan_tile<false, false, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+                for (uint32_t i = threadIdx.x; i < HW; i += kThreads) S.ring[halo_at + i] = 0u;
             }
-#endif
-            if (KMAIN == 5 && t > t0) drain_residue(S, P, t - 1, need);
         }
-        if (more) {
-            const uint32_t hb1 = ((t + 1) & 3u) * kTileWords;
-            if (edge1) init_words<kTileWords, true>(S.ring, hb1, tb + kTile, pbase, P);
-            else init_words<kTileWords, false>(S.ring, hb1, tb + kTile, pbase, P);
+        TL(1);
+        if (!waited) grid_dependency_wait();
+        waited = true;
+        {  // tile t0's words
+            const uint64_t tb = (uint64_t)t0 * kTile, hb = (t0 & 3u) * kTileWords;
+            if (t0 < ti0 || t0 >= ti1) init_words<kTileWords, true>(S.ring, hb, tb, pbase, P);
+            else init_words<kTileWords, false>(S.ring, hb, tb, pbase, P);
             pbase += kTileWords;
             if (pbase >= kPatWords) pbase -= kPatWords;
         }
         __syncthreads();
+
+        for (uint32_t t = t0; t < t1; ++t) {
+            const uint64_t tb = (uint64_t)t * kTile;
+            const uint32_t hb = (t & 3u) * kTileWords;
+            const bool edge = t < ti0 || t >= ti1;
+            // ---- X(t): clear the odd multiples of p^2, p >= 11 ----
+            // S.first[k] keeps this CTA's least slot with exponent k (its
+            // tiles come in increasing order and residue words finish in
+            // tile order); stop tracking a k once it is known.  k <= 5 come
+            // from the scan's per-tile minima of tile t - 1, k >= 6 from
+            // residue words.
+            if (FUSED && threadIdx.x >= 1 && threadIdx.x <= kDepthMax) {
+                if (threadIdx.x <= 5 && S.first_t[threadIdx.x] != ~0u) {
+                    const unsigned long long f = tb - kTile + S.first_t[threadIdx.x];
+                    if (f < S.first[threadIdx.x]) S.first[threadIdx.x] = f;
+                    S.first_t[threadIdx.x] = ~0u;
+                }
+                if (S.first[threadIdx.x] != ~0ull) atomicAnd(&S.need, ~(1u << threadIdx.x));
+            }
+            if (FUSED && threadIdx.x == 0) S.n_res[t & 1u] = 0;  // tile t - 2's queue is done
+#ifndef SQF2K_EXP_NO_SCATTER
+            scatter_medium(L, ring_addr + 4 * hb, kTile);
+            scatter_bucket(ring_addr + 4 * hb, P, t, 0);
+#endif
+            __syncthreads();
+            // ---- Y(t) ----
+            const bool more = t + 1 < t1;
+            const bool edge1 = t + 1 < ti0 || t + 1 >= ti1;
+            if (!FUSED) {
+#pragma unroll
+                for (int ch = 0; ch < kWordsPerThread / 4; ++ch) {
+                    const uint32_t w = 4 * (threadIdx.x + ch * kThreads);
+                    const uint4 v = *reinterpret_cast<const uint4 *>(&S.ring[hb + w]);
+                    *reinterpret_cast<uint4 *>(&P.bits_out[(uint64_t)t * kTileWords + w]) = v;
+                }
+            } else {
+                const uint32_t need = S.need;
+#ifndef SQF2K_EXP_NO_SCAN
+                if (need & 0x3eu) {
+                    if (edge) scan_tile<true, true, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+                    else scan_tile<false, true, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+                } else {
+                    if (edge) scan_tile<true, false, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+                    else scan_tile<false, false, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+                }
+#endif
+                if (KMAIN == 5 && t > t0) drain_residue(S, P, t - 1, need);
+            }
+            if (more) {
+                const uint32_t hb1 = ((t + 1) & 3u) * kTileWords;
+                if (edge1) init_words<kTileWords, true>(S.ring, hb1, tb + kTile, pbase, P);
+                else init_words<kTileWords, false>(S.ring, hb1, tb + kTile, pbase, P);
+                pbase += kTileWords;
+                if (pbase >= kPatWords) pbase -= kPatWords;
+            }
+            __syncthreads();
+        }
+        if (FUSED) {  // the chunk's last tile: deferred words and minima
+            if (KMAIN == 5) drain_residue(S, P, t1 - 1, S.need);
+            if (threadIdx.x >= 1 && threadIdx.x <= 5 && S.first_t[threadIdx.x] != ~0u) {
+                const unsigned long long f = (uint64_t)(t1 - 1) * kTile + S.first_t[threadIdx.x];
+                if (f < S.first[threadIdx.x]) S.first[threadIdx.x] = f;
+                S.first_t[threadIdx.x] = ~0u;
+            }
+        }
+        t0 = t1;  // take the next chunk
     }
 
-    if (FUSED) {  // the last tile's deferred words and minima, then this CTA's
-        if (KMAIN == 5) drain_residue(S, P, t1 - 1, S.need);
-        if (threadIdx.x >= 1 && threadIdx.x <= 5 && S.first_t[threadIdx.x] != ~0u) {
-            const unsigned long long f = (uint64_t)(t1 - 1) * kTile + S.first_t[threadIdx.x];
-            if (f < S.first[threadIdx.x]) S.first[threadIdx.x] = f;
-        }
+    TL(2);
+    if (FUSED) {  // this CTA's minima and counts
         __syncthreads();
         if (threadIdx.x >= 1 && threadIdx.x <= kDepthMax) {
             const unsigned long long f = S.first[threadIdx.x];
@@ -562,8 +612,22 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         if (lane == 0 && sc) atomicAdd(P.scanned, sc);
         if (threadIdx.x >= 6 && threadIdx.x <= kDepthMax && S.cnt[threadIdx.x])
             atomicAdd(&P.hist[threadIdx.x], (unsigned long long)S.cnt[threadIdx.x]);
-        if (P.acc) finish_call(S, P);
     }
+    // the last CTA resets the scheduler for the next launch and (single-batch
+    // fused calls) finishes the call
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) S.last = atomicAdd(&P.sched[1], 1u) == G - 1;
+    __syncthreads();
+    if (S.last) {
+        __threadfence();
+        if (FUSED && P.acc) finish_call(S, P);
+        if (threadIdx.x == 0) {
+            P.sched[0] = 0;
+            P.sched[1] = 0;
+        }
+    }
+    TL(3);
 }
 
 // -------------------------------------------------------------------------
@@ -666,6 +730,11 @@ void launch_tile(const char *name, unsigned grid, size_t smem, const TileParams 
     if (!attr) {
         SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<FUSED, KMAIN>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        // carve only the shared memory kCtasPerSm CTAs need: the rest stays L1,
+        // which holds the pattern table every tile reads
+        const int pct = (int)((kCtasPerSm * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+        SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<FUSED, KMAIN>,
+                                        cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         attr = true;
     }
     launch_pdl(name, tile_kernel<FUSED, KMAIN>, dim3(grid), dim3(kThreads), smem, P);
@@ -761,6 +830,11 @@ void run_tile_batch(const BatchArgs &a) {
     P.scanned = a.scanned;
     P.bits_out = a.bits_out;
     P.acc = a.fused ? a.finish_acc : nullptr;
+    if (!c.sched.ptr) {  // self-resetting scheduler words, zeroed once
+        c.sched.reserve(64);
+        SQF2K_CUDA(cudaMemset(c.sched.ptr, 0, 64));
+    }
+    P.sched = c.sched.as<unsigned int>();
     P.acc_host = a.finish_host;
     P.primes = a.primes;
     P.info = a.info;
@@ -780,5 +854,11 @@ void run_tile_batch(const BatchArgs &a) {
         launch_tile<false, 1>("tile_export", grid, smem, P);
     }
 }
+
+#ifdef SQF2K_EXP_TIMELINE
+extern "C" int sqf2k_exp_timeline(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_timeline, sizeof(g_timeline)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 }  // namespace sqf2k

@@ -53,6 +53,15 @@ constexpr int kMaxMed = 176;            // pi(1023) - 4 = 168
 constexpr int kTaskSlots = SQF2K_TASK_SLOTS;  // 32-lane scatter tasks per warp (registers)
 constexpr int kItemHits = 4;            // target hits per lane per tile
 constexpr uint32_t kPatWords = 9 * 25 * 49;  // period of the p = 3, 5, 7 pattern in words
+#ifndef SQF2K_MIN_CHUNK
+#define SQF2K_MIN_CHUNK 8
+#endif
+#ifndef SQF2K_STATIC_EIGHTHS
+#define SQF2K_STATIC_EIGHTHS 6
+#endif
+constexpr int kMinChunk = SQF2K_MIN_CHUNK;  // smallest dynamic chunk (tiles; each adds a halo)
+constexpr int kStaticEighths = SQF2K_STATIC_EIGHTHS;  // static share of the tiles, in eighths
+constexpr int kDynMinTiles = 64;        // dynamic balancing from this many tiles per CTA
 constexpr int kResCap = 256;           // deferred residue words per tile
 constexpr int kBucketCap = 64;          // fixed-capacity bucket list per tile (mean ~9)
 constexpr uint32_t kPiBelowPMed = 172;  // pi(1023): table index of the first bucket prime
@@ -110,6 +119,7 @@ struct TileParams {
     void *acc_host;
     const uint32_t *primes;
     const PrimeInfo *info;
+    unsigned int *sched;         // [0] dynamic chunks taken, [1] CTAs done (reset by the last)
 };
 
 // residue of the first slot u >= 0 with q | base_n + 2u, i.e. u = -base_n/2 mod q
