@@ -347,3 +347,17 @@ def test_single_cta_long_runs(monkeypatch, depth):
             assert got.histogram == want["histogram"], (lo, depth)
             assert got.k_sum == want["k_sum"]
             assert got.record_candidates == want["record_candidates"]
+
+
+def test_paper_full_range_to_2_50():
+    # the paper's whole computation: every odd 1 < n < 2^50,
+    # ~40 s on one B200 -- k_sum, the maximal exponent 13 and Table 3
+    s = verify_range(1, (1 << 50) + 1, 30)
+    assert s.k_sum == 684465092067182
+    assert s.k_max_observed == 13
+    assert s.failures == []
+    from paper_2411_01964_b200.aggregate import finalize_records
+    rec = finalize_records(s).entries
+    assert rec == {1: 11, 2: 29, 3: 533, 4: 849, 5: 434977, 6: 10329791, 7: 28819433,
+                   8: 129747557, 9: 6915752957, 10: 2569472629649, 11: 23373845739407,
+                   12: 60690478781437}
