@@ -44,7 +44,7 @@ __global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__res
 
 // -------------------------------------------------------------------------
 // Bucket pass: every hit u of a bucket prime (p >= kPMed, p^2 <= n_max) in the
-// batch domain [0, U), as a 16-bit offset in the list of tile u >> kTileShift.
+// batch domain [0, U), as a 16-bit offset in the list of bucket tile u >> kBucketShift.
 // Work units are (prime, sub-range) pairs of <= 5 hits (see kClasses), one
 // flat index space over all classes so each thread runs one short chain.
 //   MODE 0 (fixed): hit i of tile t goes to hits[t * kBucketCap + i]; counts
@@ -90,18 +90,18 @@ __global__ void __launch_bounds__(256) bucket_kernel(
         const uint64_t r = slot_residue(base_n, q);
         const uint64_t lm = lo % q;
         for (uint64_t u = lo + (r >= lm ? r - lm : r + q - lm); u < hi; u += q) {
-            const uint32_t t = (uint32_t)(u >> kTileShift);
+            const uint32_t t = (uint32_t)(u >> kBucketShift);
             if (MODE == 0) {
                 const uint32_t pos = atomicAdd(&counts[t], 1u);
                 if (pos < (uint32_t)kBucketCap)
-                    hits[(uint64_t)t * kBucketCap + pos] = (uint16_t)(u & (kTile - 1));
+                    hits[(uint64_t)t * kBucketCap + pos] = (uint16_t)(u & (kBucketTile - 1));
                 else
                     atomicOr(overflow, 1u);
             } else if (MODE == 1) {
                 atomicAdd(&counts[t], 1u);
             } else {
                 const uint32_t pos = offsets[t] + atomicSub(&counts[t], 1u) - 1u;
-                hits[pos] = (uint16_t)(u & (kTile - 1));
+                hits[pos] = (uint16_t)(u & (kBucketTile - 1));
             }
         }
     }
@@ -193,22 +193,27 @@ __device__ __forceinline__ void init_medium(MedLane &L, const TileParams &P, uin
 }
 
 // clear the bucket hits of tile t with offsets in [skip, kTile), shifted by
-// -skip; run by the last warp only (~5 hits per tile; build_med gives that
-// warp less medium work)
+// -skip (its kSubTiles bucket-tile lists); run by the last warp only (~9
+// hits per 2^16 slots; build_med gives that warp less medium work)
 __device__ __forceinline__ void scatter_bucket(uint32_t wbase, const TileParams &P, uint32_t t,
                                                uint32_t skip) {
     if ((threadIdx.x >> 5) != kThreads / 32 - 1) return;
-    uint32_t b, e;
-    if (P.tile_start) {
-        b = __ldg(&P.tile_start[t]);
-        e = __ldg(&P.tile_start[t + 1]);
-    } else {
-        b = t * (uint32_t)kBucketCap;
-        e = b + min(__ldg(&P.tile_count[t]), (uint32_t)kBucketCap);
-    }
-    for (uint32_t i = b + (threadIdx.x & 31); i < e; i += 32) {
-        const uint32_t o = __ldg(&P.hits[i]);
-        if (o >= skip) clear_bit(wbase, o - skip);
+#pragma unroll
+    for (int j = 0; j < kSubTiles; ++j) {
+        const uint32_t bt = t * kSubTiles + j;
+        if (bt >= P.n_btiles || (uint32_t)(j + 1) * kBucketTile <= skip) continue;
+        uint32_t b, e;
+        if (P.tile_start) {
+            b = __ldg(&P.tile_start[bt]);
+            e = __ldg(&P.tile_start[bt + 1]);
+        } else {
+            b = bt * (uint32_t)kBucketCap;
+            e = b + min(__ldg(&P.tile_count[bt]), (uint32_t)kBucketCap);
+        }
+        for (uint32_t i = b + (threadIdx.x & 31); i < e; i += 32) {
+            const uint32_t o = j * kBucketTile + __ldg(&P.hits[i]);
+            if (o >= skip) clear_bit(wbase, o - skip);
+        }
     }
 }
 
@@ -383,7 +388,7 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
 // rotating, so no warp carries them all.
 __device__ __forceinline__ void drain_residue(TileSmem &S, const TileParams &P, uint32_t tp,
                                               uint32_t need) {
-    if ((threadIdx.x >> 5) != (tp & (kThreads / 32 - 1))) return;
+    if ((threadIdx.x >> 5) != (tp & (kThreads / 32 - 1))) return;  // (warp count: power of 2)
     const uint32_t qi = tp & 1u, n = min(S.n_res[qi], (uint32_t)kResCap);
     const uint32_t hb = (tp & 3u) * kTileWords;
     for (uint32_t e = threadIdx.x & 31; e < n; e += 32) {
@@ -440,7 +445,7 @@ template <bool FUSED, int KMAIN>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TileParams P) {
     static_assert(kWordsPerThread % 4 == 0 && kThreads * kWordsPerThread == kTileWords,
                   "4-word chunks per thread");
-    static_assert(kThreads / 32 == 8, "drain_residue rotates over 8 warps");
+    static_assert(((kThreads / 32) & (kThreads / 32 - 1)) == 0, "drain_residue rotates over the warps");
     extern __shared__ __align__(16) uint8_t smem_raw[];
     TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
     const uint32_t G = gridDim.x;
@@ -745,7 +750,6 @@ void launch_tile(const char *name, unsigned grid, size_t smem, const TileParams 
 // on stream `st` (the side stream for the first batch of a call).
 void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
     Context &c = ctx();
-    const uint32_t n_tiles = (uint32_t)ceil_div(a.U, kTile);
 
     // medium tables: cached per distinct prime set
     constexpr size_t kTaskWords = (size_t)(kThreads / 32) * kTaskSlots * 64;
@@ -764,8 +768,9 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
     c.pattern.reserve((kPatWords + kTileWords) * 4);
     launch_on(st, "pattern", pattern_kernel, dim3(ceil_div(kPatWords + kTileWords, 256)), dim3(256),
               0, a.base_n, a.pattern_present, c.pattern.as<uint32_t>());
-    c.tile_counts.reserve((n_tiles + 1) * 4);
-    SQF2K_CUDA(cudaMemsetAsync(c.tile_counts.ptr, 0, (n_tiles + 1) * 4, st));
+    const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);
+    c.tile_counts.reserve((n_bt + 1) * 4);
+    SQF2K_CUDA(cudaMemsetAsync(c.tile_counts.ptr, 0, (n_bt + 1) * 4, st));
 }
 
 // Bucket lists and the tile kernel of a batch (after prep_tile_batch and the
@@ -773,28 +778,29 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
 void run_tile_batch(const BatchArgs &a) {
     Context &c = ctx();
     const uint32_t n_tiles = (uint32_t)ceil_div(a.U, kTile);
+    const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);
 
     // bucket lists (sizes bounded on the host: no sync)
     uint32_t *counts = c.tile_counts.as<uint32_t>();
     const unsigned bgrid = (unsigned)c.sm_count * 8;
     const uint32_t *tile_start = nullptr;
     if (!a.exact_buckets) {
-        c.hits.reserve((size_t)n_tiles * kBucketCap * 2 + 64);
+        c.hits.reserve((size_t)n_bt * kBucketCap * 2 + 64);
         launch("bucket_fill", bucket_kernel<0>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
                a.base_n, a.U, counts, (const uint32_t *)nullptr, c.hits.as<uint16_t>(),
                a.overflow);
     } else {
-        c.tile_offsets.reserve((n_tiles + 1) * 4);
+        c.tile_offsets.reserve((n_bt + 1) * 4);
         uint32_t *offsets = c.tile_offsets.as<uint32_t>();
         c.hits.reserve(bucket_hits_bound(a.U, a.n_primes_bound) * 2 + 64);
         launch("bucket_count", bucket_kernel<1>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
                a.base_n, a.U, counts, (const uint32_t *)offsets, (uint16_t *)nullptr, a.overflow);
         size_t tmp_bytes = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, (int)n_tiles + 1,
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, (int)n_bt + 1,
                                       c.stream);
         c.scan_tmp.reserve(std::max<size_t>(tmp_bytes, 64));
         SQF2K_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.ptr, tmp_bytes, counts, offsets,
-                                                 (int)n_tiles + 1, c.stream));
+                                                 (int)n_bt + 1, c.stream));
         launch("bucket_fill", bucket_kernel<2>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
                a.base_n, a.U, counts, (const uint32_t *)offsets, c.hits.as<uint16_t>(),
                a.overflow);
@@ -810,6 +816,7 @@ void run_tile_batch(const BatchArgs &a) {
     P.one_u = a.one_u;
     P.H = a.H;
     P.n_tiles = n_tiles;
+    P.n_btiles = n_bt;
     P.k_eff = a.k_eff;
     P.k_max = a.k_max;
 

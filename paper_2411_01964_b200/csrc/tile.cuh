@@ -33,6 +33,12 @@ namespace sqf2k {
 constexpr int kTileShift = SQF2K_TILE_SHIFT;
 constexpr int kTile = 1 << kTileShift;  // slots per tile (65536)
 constexpr int kTileWords = kTile / 32;  // 2048 packed words
+// bucket lists are kept per 2^16-slot "bucket tile" (16-bit offsets); a tile
+// holds kSubTiles of them
+constexpr int kBucketShift = 16;
+constexpr int kBucketTile = 1 << kBucketShift;
+constexpr int kSubTiles = kTile / kBucketTile;
+static_assert(kTile >= kBucketTile, "tiles are whole bucket tiles");
 #ifndef SQF2K_WORDS_PER_THREAD
 #define SQF2K_WORDS_PER_THREAD 8
 #endif
@@ -43,6 +49,12 @@ constexpr int kThreads = kTileWords / kWordsPerThread;  // CTA size
 #endif
 constexpr int kCtasPerSm = SQF2K_CTAS_PER_SM;
 constexpr int kDepthMax = 16;           // max exponent resolved in-tile
+#ifndef SQF2K_DEPTH_DEFAULT
+#define SQF2K_DEPTH_DEFAULT 16
+#endif
+// default in-tile depth (k <= 13 for every odd n < 2^50, PAPER.md:258-261;
+// 13 measured no faster, so the default keeps the widest in-tile range)
+constexpr int kDepthDefault = SQF2K_DEPTH_DEFAULT;
 constexpr int kHaloMax = 1 << (kDepthMax - 1);
 constexpr int kHaloWordsMax = kHaloMax / 32;
 constexpr uint32_t kPMed = 1024;        // medium primes: 11 <= p < kPMed
@@ -54,14 +66,17 @@ constexpr int kTaskSlots = SQF2K_TASK_SLOTS;  // 32-lane scatter tasks per warp 
 constexpr int kItemHits = 4;            // target hits per lane per tile
 constexpr uint32_t kPatWords = 9 * 25 * 49;  // period of the p = 3, 5, 7 pattern in words
 #ifndef SQF2K_MIN_CHUNK
-#define SQF2K_MIN_CHUNK 8
+#define SQF2K_MIN_CHUNK 4
 #endif
 #ifndef SQF2K_STATIC_EIGHTHS
 #define SQF2K_STATIC_EIGHTHS 6
 #endif
 constexpr int kMinChunk = SQF2K_MIN_CHUNK;  // smallest dynamic chunk (tiles; each adds a halo)
 constexpr int kStaticEighths = SQF2K_STATIC_EIGHTHS;  // static share of the tiles, in eighths
-constexpr int kDynMinTiles = 64;        // dynamic balancing from this many tiles per CTA
+#ifndef SQF2K_DYN_MIN_TILES
+#define SQF2K_DYN_MIN_TILES 64
+#endif
+constexpr int kDynMinTiles = SQF2K_DYN_MIN_TILES;  // dynamic balancing from this many tiles per CTA
 constexpr int kResCap = 256;           // deferred residue words per tile
 constexpr int kBucketCap = 64;          // fixed-capacity bucket list per tile (mean ~9)
 constexpr uint32_t kPiBelowPMed = 172;  // pi(1023): table index of the first bucket prime
@@ -94,15 +109,16 @@ struct TileParams {
     uint64_t one_u;      // slot of n = 1 if scanned (excluded), else ~0
     uint32_t H;          // halo slots (multiple of 1024; 0 in export mode)
     uint32_t n_tiles;
+    uint32_t n_btiles;   // bucket tiles (2^16 slots) in the domain
     uint32_t k_eff;      // passes inside the tile
     uint32_t k_max;      // run limit: escalate when k_max > k_eff
     const uint32_t *pattern;     // p = 3, 5, 7 mask by u-word mod kPatWords (+ kTileWords
                                  // repeated words, so a tile never wraps)
     const uint32_t *med;         // q = p^2 of the medium primes
     const uint2 *tasks;          // [warp][kTaskSlots][lane]: (m | mult << 8, step), step 0 idle
-    const uint32_t *tile_start;  // exact bucket lists: bounds, n_tiles + 1 (or null)
-    const uint32_t *tile_count;  // fixed-capacity lists: hits of tile t at t*kBucketCap
-    const uint16_t *hits;        // bucket hits, offsets within the tile
+    const uint32_t *tile_start;  // exact bucket lists: bounds, n_btiles + 1 (or null)
+    const uint32_t *tile_count;  // fixed-capacity lists: hits of bucket tile b at b*kBucketCap
+    const uint16_t *hits;        // bucket hits, offsets within the bucket tile
     unsigned long long *hist;    // [65]
     unsigned long long *min_n;   // [65]
     unsigned long long *esc;     // escalation list (n values)

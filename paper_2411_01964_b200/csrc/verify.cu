@@ -228,7 +228,7 @@ void enqueue_verify(const VerifyPlan &pl) {
     // one fused batch at the default depth: the tile kernel's last CTA does
     // the (rare) escalations and writes the accumulators to pinned memory
     const bool finish_in_tile = pl.pipeline == 0 && pl.n_slots <= pl.batch &&
-                                pl.k_eff == (uint32_t)kDepthMax;
+                                pl.k_eff >= (uint32_t)kDepthDefault;
     for (uint64_t s0 = 0; s0 < pl.n_slots; s0 += pl.batch) {
         const auto [A, sb] = set_batch(s0);
         if (s0) prep_tile_batch(a, c.stream);
@@ -334,7 +334,7 @@ void capture_graph(const VerifyPlan &pl, const uint64_t key[8]) {
 int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verify_opts_t &o,
                  sqf2k_summary_t *out, uint64_t *failures, uint64_t fail_cap) {
     Context &c = ctx();
-    const uint32_t depth = o.tile_depth ? o.tile_depth : kDepthMax;
+    const uint32_t depth = o.tile_depth ? o.tile_depth : kDepthDefault;
     if (depth < 1 || depth > (uint32_t)kDepthMax)
         return fail(SQF2K_EINVAL, "tile_depth must be in 1..%d", kDepthMax);
     VerifyPlan pl;

@@ -48,3 +48,26 @@ order = np.argsort(m)
 print("slowest SMs:", [(int(ids[i]), round(float(m[i]))) for i in order[-12:]])
 print("fastest SMs:", [(int(ids[i]), round(float(m[i]))) for i in order[:12]])
 np.save("gpurun_out/sm_loop.npy", np.stack([ids, m]))
+if g == 592:
+    waves = loop.reshape(4, 148)
+    print("loop by wave (blockIdx // 148): mean", [round(float(x), 1) for x in waves.mean(1)],
+          "min", [round(float(x), 1) for x in waves.min(1)], "max", [round(float(x), 1) for x in waves.max(1)])
+    sm_of = smid.reshape(4, 148)
+    print("same SM for b and b+148?", float((sm_of[0] == sm_of[1]).mean()), "smid of 0..7:", smid[:8].tolist(), "148..155:", smid[148:156].tolist())
+# within-SM rank by start time vs loop time
+ranks = {}
+for i in range(g):
+    ranks.setdefault(int(smid[i]), []).append(i)
+by_rank = [[], [], [], [], [], []]
+by_bidx = [[], [], [], [], [], []]
+for sm, ids in ranks.items():
+    if len(ids) > 6 or len(ids) < 1:
+        continue
+    order = sorted(ids, key=lambda i: b[i, 0])
+    for r, i in enumerate(order):
+        by_rank[r].append(loop[i])
+    for r, i in enumerate(sorted(ids)):
+        by_bidx[r].append(loop[i])
+print("group sizes", sorted(set(len(v) for v in ranks.values())))
+print("loop by start-rank on SM:", [round(float(np.mean(x)), 1) for x in by_rank if x])
+print("loop by blockIdx-rank on SM:", [round(float(np.mean(x)), 1) for x in by_bidx if x])
