@@ -58,21 +58,28 @@ __global__ void __launch_bounds__(256) bucket_kernel(
     uint64_t U, uint32_t *__restrict__ counts, const uint32_t *__restrict__ offsets,
     uint16_t *__restrict__ hits, unsigned int *__restrict__ overflow) {
     grid_dependents_launch();  // the tile kernel may start its prime-free prologue
+    static_assert(kClasses <= 32, "one lane per class");
     __shared__ unsigned long long s_end[kClasses];  // cumulative work per class
     __shared__ uint32_t s_lo[kClasses];
     __shared__ unsigned long long s_nsub[kClasses];
-    if (threadIdx.x == 0) {
-        unsigned long long acc = 0;
-        const uint32_t i_lo = info->i_lo, i_hi = info->i_hi;
-        for (int j = 0; j < kClasses; ++j) {
-            const uint32_t p_lo = max(info->cls[j], i_lo), p_hi = min(info->cls[j + 1], i_hi);
+    if (threadIdx.x < 32) {  // class table: a lane per class, warp prefix sum
+        const int j = threadIdx.x;
+        unsigned long long work = 0;
+        if (j < kClasses) {
+            const uint32_t p_lo = max(info->cls[j], info->i_lo);
+            const uint32_t p_hi = min(info->cls[j + 1], info->i_hi);
             const int sh = min(22 + 2 * j, 62);
             const unsigned long long n_sub = (U + (1ull << sh) - 1) >> sh;
             s_lo[j] = p_lo;
             s_nsub[j] = n_sub;
-            acc += p_lo < p_hi ? (unsigned long long)(p_hi - p_lo) * n_sub : 0ull;
-            s_end[j] = acc;
+            work = p_lo < p_hi ? (unsigned long long)(p_hi - p_lo) * n_sub : 0ull;
         }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long x = __shfl_up_sync(0xffffffffu, work, d);
+            if (j >= d) work += x;
+        }
+        if (j < kClasses) s_end[j] = work;
     }
     __syncthreads();
     const unsigned long long n_work = s_end[kClasses - 1];
@@ -89,19 +96,32 @@ __global__ void __launch_bounds__(256) bucket_kernel(
         const uint64_t q = p * p;
         const uint64_t r = slot_residue(base_n, q);
         const uint64_t lm = lo % q;
-        for (uint64_t u = lo + (r >= lm ? r - lm : r + q - lm); u < hi; u += q) {
-            const uint32_t t = (uint32_t)(u >> kBucketShift);
+        // <= 5 hits (q >= 2^(20+2j), range 2^(22+2j)): all atomics in flight
+        // together, then the stores -- one round trip, not one per hit
+        const uint64_t u0 = lo + (r >= lm ? r - lm : r + q - lm);
+        const int nh = u0 >= hi ? 0 : (int)min((hi - 1 - u0) / q + 1, (uint64_t)5);
+        uint32_t hu[5], pos[5];
+        uint32_t bt[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            if (i >= nh) break;
+            const uint64_t u = u0 + (uint64_t)i * q;
+            bt[i] = (uint32_t)(u >> kBucketShift);
+            hu[i] = (uint32_t)(u & (kBucketTile - 1));
+            if (MODE == 0) pos[i] = atomicAdd(&counts[bt[i]], 1u);
+            else if (MODE == 1) atomicAdd(&counts[bt[i]], 1u);
+            else pos[i] = atomicSub(&counts[bt[i]], 1u);
+        }
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            if (i >= nh) break;
             if (MODE == 0) {
-                const uint32_t pos = atomicAdd(&counts[t], 1u);
-                if (pos < (uint32_t)kBucketCap)
-                    hits[(uint64_t)t * kBucketCap + pos] = (uint16_t)(u & (kBucketTile - 1));
+                if (pos[i] < (uint32_t)kBucketCap)
+                    hits[(uint64_t)bt[i] * kBucketCap + pos[i]] = (uint16_t)hu[i];
                 else
                     atomicOr(overflow, 1u);
-            } else if (MODE == 1) {
-                atomicAdd(&counts[t], 1u);
-            } else {
-                const uint32_t pos = offsets[t] + atomicSub(&counts[t], 1u) - 1u;
-                hits[pos] = (uint16_t)(u & (kBucketTile - 1));
+            } else if (MODE == 2) {
+                hits[offsets[bt[i]] + pos[i] - 1u] = (uint16_t)hu[i];
             }
         }
     }
