@@ -17,23 +17,24 @@ namespace sqf2k {
 namespace {
 
 // -------------------------------------------------------------------------
-// p = 3, 5, 7: word g of the domain (slots 32g..32g+31) with every slot u
-// such that 9, 25 or 49 divides n(u) cleared.  Period 11025 words; the
-// first kTileWords words are repeated after the period so that a tile's
-// words [pbase, pbase + kTileWords) never wrap.
+// p = 3, 5, 7 (11): word g of the domain (slots 32g..32g+31) with every slot
+// u such that 9, 25, 49 (or 121) divides n(u) cleared.  Period kPatWords
+// words; the first kTileWords words are repeated after the period so that a
+// tile's words [pbase, pbase + kTileWords) never wrap.
 // First hit at or after 32g: y = (r - 32g) mod q; the word's hits are the
 // bits y, y+q, ... < 32, i.e. (bits 0, q, 2q, ...) << y.
 __global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__restrict__ table) {
-    const uint32_t q[3] = {9, 25, 49};
-    const uint32_t pat[3] = {0x08040201u, 0x02000001u, 0x1u};
-    uint32_t r[3];
+    constexpr int NP = kPattern11 ? 4 : 3;
+    const uint32_t q[4] = {9, 25, 49, 121};
+    const uint32_t pat[4] = {0x08040201u, 0x02000001u, 0x1u, 0x1u};
+    uint32_t r[4];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) r[i] = (uint32_t)slot_residue(base_n, q[i]);
+    for (int i = 0; i < NP; ++i) r[i] = (uint32_t)slot_residue(base_n, q[i]);
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < kPatWords + kTileWords;
          g += gridDim.x * blockDim.x) {
         uint32_t clr = 0;
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
+        for (int i = 0; i < NP; ++i) {
             if (!((present >> i) & 1u)) continue;
             const uint32_t y = (r[i] + q[i] - (32u * g) % q[i]) % q[i];
             if (y < 32) clr |= pat[i] << y;
@@ -786,7 +787,8 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
 
     // p = 3, 5, 7 pattern of this domain
     c.pattern.reserve((kPatWords + kTileWords) * 4);
-    launch_on(st, "pattern", pattern_kernel, dim3(ceil_div(kPatWords + kTileWords, 256)), dim3(256),
+    launch_on(st, "pattern", pattern_kernel,
+              dim3((unsigned)std::min<uint64_t>(ceil_div(kPatWords + kTileWords, 256), c.sm_count * 8)), dim3(256),
               0, a.base_n, a.pattern_present, c.pattern.as<uint32_t>());
     const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);
     c.tile_counts.reserve((n_bt + 1) * 4);

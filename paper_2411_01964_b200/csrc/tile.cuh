@@ -64,7 +64,14 @@ constexpr int kMaxMed = 176;            // pi(1023) - 4 = 168
 #endif
 constexpr int kTaskSlots = SQF2K_TASK_SLOTS;  // 32-lane scatter tasks per warp (registers)
 constexpr int kItemHits = 4;            // target hits per lane per tile
-constexpr uint32_t kPatWords = 9 * 25 * 49;  // period of the p = 3, 5, 7 pattern in words
+#ifndef SQF2K_PATTERN_11
+#define SQF2K_PATTERN_11 0
+#endif
+// p = 3, 5, 7 (and optionally 11: measured no faster) are applied as one
+// periodic word pattern: period
+// 9*25*49 words (*121 with 11: 1.33 M words, 5.3 MB, L2-resident)
+constexpr bool kPattern11 = SQF2K_PATTERN_11 != 0;
+constexpr uint32_t kPatWords = 9 * 25 * 49 * (kPattern11 ? 121 : 1);
 #ifndef SQF2K_MIN_CHUNK
 #define SQF2K_MIN_CHUNK 4
 #endif
@@ -112,7 +119,7 @@ struct TileParams {
     uint32_t n_btiles;   // bucket tiles (2^16 slots) in the domain
     uint32_t k_eff;      // passes inside the tile
     uint32_t k_max;      // run limit: escalate when k_max > k_eff
-    const uint32_t *pattern;     // p = 3, 5, 7 mask by u-word mod kPatWords (+ kTileWords
+    const uint32_t *pattern;     // p = 3, 5, 7 (11) mask by u-word mod kPatWords (+ kTileWords
                                  // repeated words, so a tile never wraps)
     const uint32_t *med;         // q = p^2 of the medium primes
     const uint2 *tasks;          // [warp][kTaskSlots][lane]: (m | mult << 8, step), step 0 idle
@@ -159,7 +166,7 @@ struct BatchArgs {
     const uint32_t *primes;       // device table
     const PrimeInfo *info;        // device split
     uint64_t n_primes_bound;      // host upper bound of the table size
-    uint32_t pattern_present;     // bit i: prime 3/5/7 in the table
+    uint32_t pattern_present;     // bit i: prime 3/5/7/11 in the table
     const std::vector<uint32_t> *med_primes;
     unsigned long long *hist, *min_n, *esc, *esc_count, *fail, *fail_count;
     uint64_t esc_cap, fail_cap;

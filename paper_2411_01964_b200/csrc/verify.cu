@@ -93,7 +93,7 @@ unsigned warp_grid(uint64_t items) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(items, 8), cap));
 }
 
-// Medium primes and the p = 3, 5, 7 presence of "all primes <= limit".
+// Medium primes and the p = 3, 5, 7 (11) presence of "all primes <= limit".
 struct SmallSet {
     std::vector<uint32_t> med;
     uint32_t present = 0;
@@ -107,6 +107,7 @@ SmallSet small_set_upto(uint64_t limit) {
         if (p == 3) s.present |= 1;
         else if (p == 5) s.present |= 2;
         else if (p == 7) s.present |= 4;
+        else if (p == 11 && kPattern11) s.present |= 8;
         else if (p >= 11) s.med.push_back(p);
     }
     return s;
@@ -450,6 +451,7 @@ int sieve_bits(uint64_t start, uint64_t end, const int64_t *primes_h, uint64_t n
         if (p == 3) small.present |= 1;
         else if (p == 5) small.present |= 2;
         else if (p == 7) small.present |= 4;
+        else if (p == 11 && kPattern11) small.present |= 8;
         else if (p >= 11) small.med.push_back(p);
     }
     const uint32_t nt = (uint32_t)ceil_div(n_slots, kTile);

@@ -52,3 +52,33 @@ for k, (n, ms) in sorted(st.items(), key=lambda kv: -kv[1][1]):
     print(f"  {k:16s} {n / N:4.1f}/call {ms / N * 1e3:8.1f} us")
     tot += ms / N * 1e3
 print(f"kernel sum (event per launch): {tot:.1f} us")
+# the same call right after an L2 flush (as bench.py's timed steps)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for mode in ("zero_", "fill_read"):
+    ts = []
+    for _ in range(N):
+        if mode == "zero_":
+            flush.zero_()
+        else:
+            flush.zero_()
+            _ = int(flush[::4096].sum())  # read back: L2 holds clean lines
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        L.sqf2k_verify(lo, hi, 30, ctypes.byref(opts), ctypes.byref(s), _lib.ptr(fail), 4096)
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    print(f"after L2 flush ({mode}): {sum(ts) / N:8.1f} us (min {min(ts):.1f})")
+_lib.profile(True)
+for fl in (False, True):
+    _lib.profile_reset()
+    for _ in range(N):
+        if fl:
+            flush.zero_()
+        torch.cuda.synchronize()
+        verify_range(lo, hi, 30)
+    st = _lib.profile_read()
+    print("flush" if fl else "no flush", {k: round(ms / N * 1e3, 1) for k, (n, ms) in st.items()})
+_lib.profile(False)
