@@ -563,15 +563,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             // tile order); stop tracking a k once it is known.  k <= 5 come
             // from the scan's per-tile minima of tile t - 1, k >= 6 from
             // residue words.
-            if (FUSED && threadIdx.x >= 1 && threadIdx.x <= kDepthMax) {
-                if (threadIdx.x <= 5 && S.first_t[threadIdx.x] != ~0u) {
-                    const unsigned long long f = tb - kTile + S.first_t[threadIdx.x];
-                    if (f < S.first[threadIdx.x]) S.first[threadIdx.x] = f;
-                    S.first_t[threadIdx.x] = ~0u;
+            if (FUSED && threadIdx.x < 32) {  // bookkeeping: warp 0 only (uniform branch)
+                const uint32_t k = threadIdx.x;
+                if (k >= 1 && k <= 5 && S.first_t[k] != ~0u) {
+                    const unsigned long long f = tb - kTile + S.first_t[k];
+                    if (f < S.first[k]) S.first[k] = f;
+                    S.first_t[k] = ~0u;
                 }
-                if (S.first[threadIdx.x] != ~0ull) atomicAnd(&S.need, ~(1u << threadIdx.x));
+                const uint32_t known =
+                    __ballot_sync(0xffffffffu, k >= 1 && k <= kDepthMax && S.first[k] != ~0ull);
+                if (k == 0) {
+                    S.need &= ~known;
+                    S.n_res[t & 1u] = 0;  // tile t - 2's queue is done
+                }
             }
-            if (FUSED && threadIdx.x == 0) S.n_res[t & 1u] = 0;  // tile t - 2's queue is done
 #ifndef SQF2K_EXP_NO_SCATTER
             scatter_medium(L, ring_addr + 4 * hb, kTile);
             scatter_bucket(ring_addr + 4 * hb, P, t, 0);
