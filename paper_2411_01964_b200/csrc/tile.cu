@@ -138,11 +138,17 @@ __global__ void __launch_bounds__(256) bucket_kernel(
 // their hits with shared-memory atomics (random scatter: bank-conflict bound
 // at ~9 lanes/cycle/SM on B200, the same rate as byte stores, so no byte
 // array and no pack pass).
-constexpr int kRingWords = 4 * kTileWords;  // power of two
+constexpr int kRingTiles = 5;  // tiles t-2 .. t+2 are live in one phase
+constexpr int kRingWords = kRingTiles * kTileWords;
+__device__ __forceinline__ uint32_t ring_base(uint32_t t) { return (t % kRingTiles) * kTileWords; }
+// ring word i - d (d <= kTileWords), wrapping below 0
+__device__ __forceinline__ uint32_t ring_back(uint32_t i, uint32_t d) {
+    return i >= d ? i - d : i + kRingWords - d;
+}
 struct TileSmem {
     uint32_t ring[kRingWords];
     unsigned long long first[kDepthMax + 1];
-    uint32_t first_t[6];          // k <= 5: least tile-local slot in the last tracked tile
+    uint32_t first_t[2][6];       // k <= 5: least tile-local slot of tile t (buffer t & 1)
     uint32_t cnt[kDepthMax + 1];  // counts of k >= 6 (rare)
     uint32_t need;
     // words left after the main passes of tile t (queue t & 1), finished
@@ -297,7 +303,7 @@ __device__ __noinline__ void spill_word(uint32_t pend, uint64_t u0, int64_t base
 __device__ __forceinline__ void scan_residue(TileSmem &S, const TileParams &P, uint32_t hb,
                                              uint32_t w, uint64_t u0, uint32_t pend, uint32_t need) {
     for (uint32_t k = 6; k <= P.k_eff && pend; ++k) {
-        const uint32_t sl = S.ring[(hb + w - (1u << (k - 6))) & (kRingWords - 1)];
+        const uint32_t sl = S.ring[ring_back(hb + w, 1u << (k - 6))];
         const uint32_t nw = pend & sl;
         if (nw) {
             atomicAdd(&S.cnt[k], (uint32_t)__popc(nw));
@@ -317,12 +323,12 @@ __device__ __forceinline__ void scan_residue(TileSmem &S, const TileParams &P, u
 // per warp; all lanes execute the scan together).
 template <bool TRACK, bool COUNT>
 __device__ __forceinline__ void pass(uint32_t &pend, uint32_t sl, uint32_t &cnt, int k,
-                                     uint32_t need, uint32_t wl, TileSmem &S) {
+                                     uint32_t need, uint32_t wl, TileSmem &S, uint32_t qi) {
     const uint32_t nw = pend & sl;
     if (COUNT) cnt += __popc(nw);
     if (TRACK && ((need >> k) & 1u)) {
         const uint32_t m = __reduce_min_sync(0xffffffffu, nw ? 32 * wl + __ffs(nw) - 1 : ~0u);
-        if (m != ~0u && (threadIdx.x & 31) == 0) atomicMin(&S.first_t[k], m);
+        if (m != ~0u && (threadIdx.x & 31) == 0) atomicMin(&S.first_t[qi][k], m);
     }
     pend &= ~sl;
 }
@@ -333,12 +339,12 @@ __device__ __forceinline__ void pass(uint32_t &pend, uint32_t sl, uint32_t &cnt,
 template <bool TRACK, int KMAIN>
 __device__ __forceinline__ uint32_t scan_word(uint32_t pend, uint32_t prv, uint32_t cur,
                                               uint32_t (&c)[6], uint32_t need, uint32_t wl,
-                                              TileSmem &S) {
-    pass<TRACK, false>(pend, __funnelshift_l(prv, cur, 1), c[1], 1, need, wl, S);
-    if (KMAIN >= 2) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 2), c[2], 2, need, wl, S);
-    if (KMAIN >= 3) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 4), c[3], 3, need, wl, S);
-    if (KMAIN >= 4) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 8), c[4], 4, need, wl, S);
-    if (KMAIN >= 5) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 16), c[5], 5, need, wl, S);
+                                              TileSmem &S, uint32_t qi) {
+    pass<TRACK, false>(pend, __funnelshift_l(prv, cur, 1), c[1], 1, need, wl, S, qi);
+    if (KMAIN >= 2) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 2), c[2], 2, need, wl, S, qi);
+    if (KMAIN >= 3) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 4), c[3], 3, need, wl, S, qi);
+    if (KMAIN >= 4) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 8), c[4], 4, need, wl, S, qi);
+    if (KMAIN >= 5) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 16), c[5], 5, need, wl, S, qi);
     return pend;
 }
 
@@ -354,7 +360,7 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
     constexpr int W = kWordsPerThread;
     static_assert(W % 4 == 0, "4-word chunks");
     const uint32_t wt = W * threadIdx.x;
-    uint32_t prv_in = S.ring[(hb + wt - 1) & (kRingWords - 1)];
+    uint32_t prv_in = S.ring[ring_back(hb + wt, 1u)];
 #pragma unroll
     for (int ch = 0; ch < W / 4; ++ch) {
         const uint32_t w0 = wt + 4 * ch;
@@ -377,7 +383,7 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
                 }
                 scanned += __popc(pend);
             }
-            left[i] = scan_word<TRACK, KMAIN>(pend, prv[i], cur[i], c, need, w0 + i, S);
+            left[i] = scan_word<TRACK, KMAIN>(pend, prv[i], cur[i], c, need, w0 + i, S, qi);
             any |= left[i];
         }
         if (!EDGE) scanned += 128;
@@ -404,18 +410,20 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
     }
 }
 
-// Finish the deferred words of tile tp (queue tp & 1; its ring quarter and
-// the halo below stay intact until tile tp + 3 starts).  One warp per tile,
-// rotating, so no warp carries them all.
+// Finish the deferred words of tile tp (queue tp & 1; its ring buffer and
+// the one below stay intact until tile tp + 3 starts) and empty the queue.
+// One warp per tile, rotating, so no warp carries them all.
 __device__ __forceinline__ void drain_residue(TileSmem &S, const TileParams &P, uint32_t tp,
                                               uint32_t need) {
     if ((threadIdx.x >> 5) != (tp & (kThreads / 32 - 1))) return;  // (warp count: power of 2)
     const uint32_t qi = tp & 1u, n = min(S.n_res[qi], (uint32_t)kResCap);
-    const uint32_t hb = (tp & 3u) * kTileWords;
+    const uint32_t hb = ring_base(tp);
     for (uint32_t e = threadIdx.x & 31; e < n; e += 32) {
         const uint32_t w = S.res_w[qi][e];
         scan_residue(S, P, hb, w, (uint64_t)tp * kTile + 32ull * w, S.res_p[qi][e], need);
     }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) S.n_res[qi] = 0;  // free for tile tp + 2 (next phase on)
 }
 
 // Last-CTA epilogue of a single-batch call (run by the CTA that finished
@@ -496,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         S.first[threadIdx.x] = ~0ull;
         S.cnt[threadIdx.x] = 0;
     }
-    if (threadIdx.x < 6) S.first_t[threadIdx.x] = ~0u;
+    if (threadIdx.x < 12) S.first_t[threadIdx.x / 6][threadIdx.x % 6] = ~0u;
     if (threadIdx.x == 0) S.need = ~0u;
     const uint32_t ring_addr = smem_addr(S.ring);
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
@@ -523,10 +531,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         MedLane L;
         init_medium(L, P, b0);
         if (threadIdx.x < 2) S.n_res[threadIdx.x] = 0;
-        uint32_t pbase = (uint32_t)((b0 / 32) % kPatWords);
+        uint32_t pbase = (uint32_t)((b0 / 32) % kPatWords);  // pattern index of the next start
+        auto start_tile = [&](uint32_t t) {  // tile t's words from the pattern
+            const uint64_t tb = (uint64_t)t * kTile;
+            if (t < ti0 || t >= ti1) init_words<kTileWords, true>(S.ring, ring_base(t), tb, pbase, P);
+            else init_words<kTileWords, false>(S.ring, ring_base(t), tb, pbase, P);
+            pbase += kTileWords;
+            if (pbase >= kPatWords) pbase -= kPatWords;
+        };
 
-        // the halo just below tile t0: the tail of quarter (t0 - 1) & 3
-        const uint32_t halo_at = ((t0 + 3u) & 3u) * kTileWords + kTileWords - HW;
+        // the halo just below tile t0: the tail of buffer t0 - 1
+        const uint32_t halo_at = ring_base(t0 + kRingTiles - 1) + kTileWords - HW;
         if (FUSED) {
             if (pre) {  // pre-tile: sieve the H slots below the chunk
                 init_halo(S.ring, halo_at, HW, b0, pbase, P);
@@ -544,47 +559,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         TL(1);
         if (!waited) grid_dependency_wait();
         waited = true;
-        {  // tile t0's words
-            const uint64_t tb = (uint64_t)t0 * kTile, hb = (t0 & 3u) * kTileWords;
-            if (t0 < ti0 || t0 >= ti1) init_words<kTileWords, true>(S.ring, hb, tb, pbase, P);
-            else init_words<kTileWords, false>(S.ring, hb, tb, pbase, P);
-            pbase += kTileWords;
-            if (pbase >= kPatWords) pbase -= kPatWords;
-        }
+        // prologue: start t0; sieve t0 and start t0 + 1
+        start_tile(t0);
+        __syncthreads();
+        scatter_medium(L, ring_addr + 4 * ring_base(t0), kTile);
+        scatter_bucket(ring_addr + 4 * ring_base(t0), P, t0, 0);
+        if (t0 + 1 < t1) start_tile(t0 + 1);
         __syncthreads();
 
+        // One phase per tile t, one barrier: scan t (reads t and the tail of
+        // t - 1), finish t - 1's deferred words (t - 1, t - 2), sieve t + 1
+        // (started last phase), start t + 2 -- five ring buffers, disjoint.
         for (uint32_t t = t0; t < t1; ++t) {
             const uint64_t tb = (uint64_t)t * kTile;
-            const uint32_t hb = (t & 3u) * kTileWords;
+            const uint32_t hb = ring_base(t);
             const bool edge = t < ti0 || t >= ti1;
-            // ---- X(t): clear the odd multiples of p^2, p >= 11 ----
-            // S.first[k] keeps this CTA's least slot with exponent k (its
-            // tiles come in increasing order and residue words finish in
-            // tile order); stop tracking a k once it is known.  k <= 5 come
-            // from the scan's per-tile minima of tile t - 1, k >= 6 from
-            // residue words.
-            if (FUSED && threadIdx.x < 32) {  // bookkeeping: warp 0 only (uniform branch)
-                const uint32_t k = threadIdx.x;
-                if (k >= 1 && k <= 5 && S.first_t[k] != ~0u) {
-                    const unsigned long long f = tb - kTile + S.first_t[k];
-                    if (f < S.first[k]) S.first[k] = f;
-                    S.first_t[k] = ~0u;
-                }
-                const uint32_t known =
-                    __ballot_sync(0xffffffffu, k >= 1 && k <= kDepthMax && S.first[k] != ~0ull);
-                if (k == 0) {
-                    S.need &= ~known;
-                    S.n_res[t & 1u] = 0;  // tile t - 2's queue is done
-                }
-            }
-#ifndef SQF2K_EXP_NO_SCATTER
-            scatter_medium(L, ring_addr + 4 * hb, kTile);
-            scatter_bucket(ring_addr + 4 * hb, P, t, 0);
-#endif
-            __syncthreads();
-            // ---- Y(t) ----
-            const bool more = t + 1 < t1;
-            const bool edge1 = t + 1 < ti0 || t + 1 >= ti1;
             if (!FUSED) {
 #pragma unroll
                 for (int ch = 0; ch < kWordsPerThread / 4; ++ch) {
@@ -594,6 +583,22 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                 }
             } else {
                 const uint32_t need = S.need;
+                // S.first[k] keeps this CTA's least slot with exponent k (its
+                // tiles come in increasing order and residue words finish in
+                // tile order); stop tracking a k once it is known.  k <= 5
+                // come from the scan's per-tile minima (tile t - 1's buffer
+                // here), k >= 6 from residue words.
+                if (threadIdx.x < 32) {  // bookkeeping: warp 0 only (uniform branch)
+                    const uint32_t k = threadIdx.x, qp = (t + 1) & 1u;
+                    if (k >= 1 && k <= 5 && S.first_t[qp][k] != ~0u) {
+                        const unsigned long long f = tb - kTile + S.first_t[qp][k];
+                        if (f < S.first[k]) S.first[k] = f;
+                        S.first_t[qp][k] = ~0u;
+                    }
+                    const uint32_t known =
+                        __ballot_sync(0xffffffffu, k >= 1 && k <= kDepthMax && S.first[k] != ~0ull);
+                    if (k == 0) S.need &= ~known;
+                }
 #ifndef SQF2K_EXP_NO_SCAN
                 if (need & 0x3eu) {
                     if (edge) scan_tile<true, true, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
@@ -605,21 +610,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
 #endif
                 if (KMAIN == 5 && t > t0) drain_residue(S, P, t - 1, need);
             }
-            if (more) {
-                const uint32_t hb1 = ((t + 1) & 3u) * kTileWords;
-                if (edge1) init_words<kTileWords, true>(S.ring, hb1, tb + kTile, pbase, P);
-                else init_words<kTileWords, false>(S.ring, hb1, tb + kTile, pbase, P);
-                pbase += kTileWords;
-                if (pbase >= kPatWords) pbase -= kPatWords;
+            if (t + 1 < t1) {
+                const uint32_t hb1 = ring_base(t + 1);
+#ifndef SQF2K_EXP_NO_SCATTER
+                scatter_medium(L, ring_addr + 4 * hb1, kTile);
+                scatter_bucket(ring_addr + 4 * hb1, P, t + 1, 0);
+#endif
+                if (t + 2 < t1) start_tile(t + 2);
             }
             __syncthreads();
         }
         if (FUSED) {  // the chunk's last tile: deferred words and minima
             if (KMAIN == 5) drain_residue(S, P, t1 - 1, S.need);
-            if (threadIdx.x >= 1 && threadIdx.x <= 5 && S.first_t[threadIdx.x] != ~0u) {
-                const unsigned long long f = (uint64_t)(t1 - 1) * kTile + S.first_t[threadIdx.x];
+            const uint32_t ql = (t1 - 1) & 1u;
+            if (threadIdx.x >= 1 && threadIdx.x <= 5 && S.first_t[ql][threadIdx.x] != ~0u) {
+                const unsigned long long f = (uint64_t)(t1 - 1) * kTile + S.first_t[ql][threadIdx.x];
                 if (f < S.first[threadIdx.x]) S.first[threadIdx.x] = f;
-                S.first_t[threadIdx.x] = ~0u;
+                S.first_t[ql][threadIdx.x] = ~0u;
             }
         }
         t0 = t1;  // take the next chunk
