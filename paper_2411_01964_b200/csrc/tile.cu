@@ -149,8 +149,8 @@ struct TileSmem {
     uint32_t ring[kRingWords];
     unsigned long long first[kDepthMax + 1];
     uint32_t first_t[2][6];       // k <= 5: least tile-local slot of tile t (buffer t & 1)
+    uint32_t need;                // bit k: least n with exponent k still unknown
     uint32_t cnt[kDepthMax + 1];  // counts of k >= 6 (rare)
-    uint32_t need;
     // words left after the main passes of tile t (queue t & 1), finished
     // while tile t + 1 is scanned
     uint32_t res_w[2][kResCap], res_p[2][kResCap];
@@ -319,17 +319,16 @@ __device__ __forceinline__ void scan_residue(TileSmem &S, const TileParams &P, u
 
 // One pass of the main scan on one word; k = 1 is not counted (hist[1] is
 // derived from the scanned-slot count by conservation, see verify.cu).
-// TRACK: the warp's least slot with exponent k (one REDUX, one 32-bit atomic
-// per warp; all lanes execute the scan together).
+// One pass of the main scan on one word; k = 1 is not counted (hist[1] is
+// derived from the scanned-slot count by conservation, see verify.cu).
+// TRACK: the thread's least slot with exponent k (its words come in slot
+// order, so the first hit is the least); reduced per warp after the tile.
 template <bool TRACK, bool COUNT>
-__device__ __forceinline__ void pass(uint32_t &pend, uint32_t sl, uint32_t &cnt, int k,
-                                     uint32_t need, uint32_t wl, TileSmem &S, uint32_t qi) {
+__device__ __forceinline__ void pass(uint32_t &pend, uint32_t sl, uint32_t &cnt, uint32_t &fk,
+                                     uint32_t wl) {
     const uint32_t nw = pend & sl;
     if (COUNT) cnt += __popc(nw);
-    if (TRACK && ((need >> k) & 1u)) {
-        const uint32_t m = __reduce_min_sync(0xffffffffu, nw ? 32 * wl + __ffs(nw) - 1 : ~0u);
-        if (m != ~0u && (threadIdx.x & 31) == 0) atomicMin(&S.first_t[qi][k], m);
-    }
+    if (TRACK && nw && fk == ~0u) fk = 32 * wl + __ffs(nw) - 1;
     pend &= ~sl;
 }
 
@@ -338,13 +337,12 @@ __device__ __forceinline__ void pass(uint32_t &pend, uint32_t sl, uint32_t &cnt,
 // passes.
 template <bool TRACK, int KMAIN>
 __device__ __forceinline__ uint32_t scan_word(uint32_t pend, uint32_t prv, uint32_t cur,
-                                              uint32_t (&c)[6], uint32_t need, uint32_t wl,
-                                              TileSmem &S, uint32_t qi) {
-    pass<TRACK, false>(pend, __funnelshift_l(prv, cur, 1), c[1], 1, need, wl, S, qi);
-    if (KMAIN >= 2) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 2), c[2], 2, need, wl, S, qi);
-    if (KMAIN >= 3) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 4), c[3], 3, need, wl, S, qi);
-    if (KMAIN >= 4) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 8), c[4], 4, need, wl, S, qi);
-    if (KMAIN >= 5) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 16), c[5], 5, need, wl, S, qi);
+                                              uint32_t (&c)[6], uint32_t (&f)[6], uint32_t wl) {
+    pass<TRACK, false>(pend, __funnelshift_l(prv, cur, 1), c[1], f[1], wl);
+    if (KMAIN >= 2) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 2), c[2], f[2], wl);
+    if (KMAIN >= 3) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 4), c[3], f[3], wl);
+    if (KMAIN >= 4) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 8), c[4], f[4], wl);
+    if (KMAIN >= 5) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 16), c[5], f[5], wl);
     return pend;
 }
 
@@ -360,6 +358,7 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
     constexpr int W = kWordsPerThread;
     static_assert(W % 4 == 0, "4-word chunks");
     const uint32_t wt = W * threadIdx.x;
+    uint32_t f[6] = {~0u, ~0u, ~0u, ~0u, ~0u, ~0u};  // TRACK: least tile-local slot per k
     uint32_t prv_in = S.ring[ring_back(hb + wt, 1u)];
 #pragma unroll
     for (int ch = 0; ch < W / 4; ++ch) {
@@ -383,7 +382,7 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
                 }
                 scanned += __popc(pend);
             }
-            left[i] = scan_word<TRACK, KMAIN>(pend, prv[i], cur[i], c, need, w0 + i, S, qi);
+            left[i] = scan_word<TRACK, KMAIN>(pend, prv[i], cur[i], c, f, w0 + i);
             any |= left[i];
         }
         if (!EDGE) scanned += 128;
@@ -406,6 +405,14 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
                     spill_word(left[i], u0, P.base_n, P.fail, P.fail_count, P.fail_cap);
                 }
             }
+        }
+    }
+    if (TRACK) {  // per k: one warp reduction, one shared atomic
+#pragma unroll
+        for (int k = 1; k <= KMAIN; ++k) {
+            if (!((need >> k) & 1u)) continue;
+            const uint32_t m = __reduce_min_sync(0xffffffffu, f[k]);
+            if (m != ~0u && (threadIdx.x & 31) == 0) atomicMin(&S.first_t[qi][k], m);
         }
     }
 }
@@ -466,8 +473,17 @@ __device__ __forceinline__ void tl_mark(int i) {
     }
 }
 #define TL(i) tl_mark(i)
+__device__ unsigned long long g_tiles[8][64];
+__device__ __forceinline__ void tl_tile(uint32_t i) {
+    if (threadIdx.x != 0 || blockIdx.x >= 8 || i >= 64) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tiles[blockIdx.x][i] = t;
+}
+#define TLT(i) tl_tile(i)
 #else
 #define TL(i) do { } while (0)
+#define TLT(i) do { } while (0)
 #endif
 
 template <bool FUSED, int KMAIN>
@@ -582,12 +598,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                     *reinterpret_cast<uint4 *>(&P.bits_out[(uint64_t)t * kTileWords + w]) = v;
                 }
             } else {
-                const uint32_t need = S.need;
                 // S.first[k] keeps this CTA's least slot with exponent k (its
                 // tiles come in increasing order and residue words finish in
-                // tile order); stop tracking a k once it is known.  k <= 5
-                // come from the scan's per-tile minima (tile t - 1's buffer
-                // here), k >= 6 from residue words.
+                // tile order); stop tracking a k once it is known (warp 0 folds
+                // tile t - 1's scan minima into S.first and clears S.need bits
+                // in this phase: a stale read only tracks once more).
+                const uint32_t need = S.need;
                 if (threadIdx.x < 32) {  // bookkeeping: warp 0 only (uniform branch)
                     const uint32_t k = threadIdx.x, qp = (t + 1) & 1u;
                     if (k >= 1 && k <= 5 && S.first_t[qp][k] != ~0u) {
@@ -619,6 +635,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                 if (t + 2 < t1) start_tile(t + 2);
             }
             __syncthreads();
+            TLT(t - t0);
         }
         if (FUSED) {  // the chunk's last tile: deferred words and minima
             if (KMAIN == 5) drain_residue(S, P, t1 - 1, S.need);
@@ -899,6 +916,9 @@ void run_tile_batch(const BatchArgs &a) {
 #ifdef SQF2K_EXP_TIMELINE
 extern "C" int sqf2k_exp_timeline(unsigned long long *out) {
     return cudaMemcpyFromSymbol(out, g_timeline, sizeof(g_timeline)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int sqf2k_exp_tiles(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_tiles, sizeof(g_tiles)) == cudaSuccess ? 0 : -1;
 }
 #endif
 
