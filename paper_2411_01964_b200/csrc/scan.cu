@@ -102,20 +102,11 @@ __device__ void wscan_residue(const ScanParams &P, const uint32_t *__restrict__ 
 // the range and n = 1.  The common path (neither) is ~18 ops per 32 slots.
 template <int KMAIN, bool TRACK, bool EDGE>
 __device__ __forceinline__ void wscan_group(const ScanParams &P, const uint32_t *__restrict__ w,
-                                            uint64_t g, uint64_t word0, uint32_t (&c)[6],
+                                            uint64_t g, uint64_t word0, const uint32_t (&cur)[kGroupWords],
+                                            uint32_t prv, uint32_t (&c)[6],
                                             unsigned long long &scanned, uint32_t &tneed,
                                             uint32_t *s_cnt, unsigned long long *s_first) {
     const uint64_t wg = word0 + g * kGroupWords;
-    uint32_t cur[kGroupWords];
-#pragma unroll
-    for (int v = 0; v < kGroupWords / 4; ++v) {
-        const uint4 x = P.w4[wg / 4 + v];
-        cur[4 * v] = x.x;
-        cur[4 * v + 1] = x.y;
-        cur[4 * v + 2] = x.z;
-        cur[4 * v + 3] = x.w;
-    }
-    uint32_t prv = w[wg - 1];
     const uint64_t s0 = g * 32 * kGroupWords;  // first slot of the group
     uint32_t which = 0;  // words still pending after the main passes
 #pragma unroll
@@ -148,6 +139,19 @@ __device__ __forceinline__ void wscan_group(const ScanParams &P, const uint32_t 
     }
 }
 
+// the group's words (2 x LDG.128); lanes hold consecutive groups
+__device__ __forceinline__ void wscan_load(const ScanParams &P, uint64_t wg,
+                                           uint32_t (&cur)[kGroupWords]) {
+#pragma unroll
+    for (int v = 0; v < kGroupWords / 4; ++v) {
+        const uint4 x = __ldcs(&P.w4[wg / 4 + v]);  // streamed once
+        cur[4 * v] = x.x;
+        cur[4 * v + 1] = x.y;
+        cur[4 * v + 2] = x.z;
+        cur[4 * v + 3] = x.w;
+    }
+}
+
 template <int KMAIN>
 __global__ void __launch_bounds__(kFastThreads) wscan_kernel(const ScanParams P) {
     __shared__ unsigned long long s_first[65];
@@ -167,13 +171,32 @@ __global__ void __launch_bounds__(kFastThreads) wscan_kernel(const ScanParams P)
     uint32_t tneed = (2u << KMAIN) - 2u;  // k = 1..KMAIN not met yet by this thread
     const uint64_t g_edge = P.n_slots / (32 * kGroupWords);  // groups >= this touch the end
     const uint64_t g_one = P.one_slot == ~0ull ? ~0ull : P.one_slot / (32 * kGroupWords);
-    for (uint64_t g = g_lo + threadIdx.x; g < g_hi; g += blockDim.x) {
-        if (g >= g_edge || g == g_one)
-            wscan_group<KMAIN, true, true>(P, w, g, word0, c, scanned, tneed, s_cnt, s_first);
-        else if (tneed)
-            wscan_group<KMAIN, true, false>(P, w, g, word0, c, scanned, tneed, s_cnt, s_first);
-        else
-            wscan_group<KMAIN, false, false>(P, w, g, word0, c, scanned, tneed, s_cnt, s_first);
+    const uint32_t lane = threadIdx.x & 31;
+    // software pipeline: the next iteration's words are in flight while this
+    // one is scanned; the left neighbour word comes from the lane before
+    // (consecutive groups), lane 0 loads it
+    uint32_t nxt[kGroupWords];
+    uint64_t g = g_lo + threadIdx.x;
+    const uint64_t g_first = g_lo + (threadIdx.x & ~31u);  // this warp's first group
+    if (g_first < g_hi) {
+        if (g < g_hi) wscan_load(P, word0 + g * kGroupWords, nxt);
+    }
+    for (uint64_t gw = g_first; gw < g_hi; gw += blockDim.x, g += blockDim.x) {
+        uint32_t cur[kGroupWords];
+#pragma unroll
+        for (int i = 0; i < kGroupWords; ++i) cur[i] = nxt[i];
+        const bool live = g < g_hi;
+        uint32_t prv = __shfl_up_sync(0xffffffffu, cur[kGroupWords - 1], 1);
+        if (lane == 0 && live) prv = w[word0 + g * kGroupWords - 1];
+        if (g + blockDim.x < g_hi) wscan_load(P, word0 + (g + blockDim.x) * kGroupWords, nxt);
+        if (live) {
+            if (g >= g_edge || g == g_one)
+                wscan_group<KMAIN, true, true>(P, w, g, word0, cur, prv, c, scanned, tneed, s_cnt, s_first);
+            else if (tneed)
+                wscan_group<KMAIN, true, false>(P, w, g, word0, cur, prv, c, scanned, tneed, s_cnt, s_first);
+            else
+                wscan_group<KMAIN, false, false>(P, w, g, word0, cur, prv, c, scanned, tneed, s_cnt, s_first);
+        }
     }
 #pragma unroll
     for (int k = 2; k <= 5; ++k) {
