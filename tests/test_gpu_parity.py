@@ -361,3 +361,19 @@ def test_paper_full_range_to_2_50():
     assert rec == {1: 11, 2: 29, 3: 533, 4: 849, 5: 434977, 6: 10329791, 7: 28819433,
                    8: 129747557, 9: 6915752957, 10: 2569472629649, 11: 23373845739407,
                    12: 60690478781437}
+
+
+@pytest.mark.parametrize("grid", ["3", "5"])
+def test_dynamic_chunks_against_oracle(monkeypatch, grid):
+    # a handful of CTAs over hundreds of tiles: the static share, the
+    # atomically handed-out chunks (each with its own halo pre-tile) and the
+    # scheduler reset between launches all run, on both pipelines
+    monkeypatch.setenv("SQF2K_DEBUG_GRID", grid)
+    for lo, tiles in [(1, 400), ((1 << 44) + 3, 333)]:
+        hi = lo + 2 * tiles * 65536 + 2 * 4321
+        want = O.verify(lo, hi, width=1 << 30, k_max=30)
+        for pipeline in ("fused", "bitmap"):
+            for _ in range(2):
+                got = verify_range(lo, hi, 30, pipeline=pipeline)
+                assert got.histogram == want["histogram"], (lo, grid, pipeline)
+                assert got.record_candidates == want["record_candidates"]
