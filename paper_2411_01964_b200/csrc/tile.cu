@@ -359,7 +359,7 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
     static_assert(W % 4 == 0, "4-word chunks");
     const uint32_t wt = W * threadIdx.x;
     uint32_t f[6] = {~0u, ~0u, ~0u, ~0u, ~0u, ~0u};  // TRACK: least tile-local slot per k
-    uint32_t prv_in = S.ring[ring_back(hb + wt, 1u)];
+    uint32_t prv_in = S.ring[hb + wt ? hb + wt - 1 : kRingWords - 1];
 #pragma unroll
     for (int ch = 0; ch < W / 4; ++ch) {
         const uint32_t w0 = wt + 4 * ch;
@@ -548,10 +548,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         init_medium(L, P, b0);
         if (threadIdx.x < 2) S.n_res[threadIdx.x] = 0;
         uint32_t pbase = (uint32_t)((b0 / 32) % kPatWords);  // pattern index of the next start
-        auto start_tile = [&](uint32_t t) {  // tile t's words from the pattern
+        auto start_tile = [&](uint32_t t, uint32_t at) {  // tile t's words (ring base at)
             const uint64_t tb = (uint64_t)t * kTile;
-            if (t < ti0 || t >= ti1) init_words<kTileWords, true>(S.ring, ring_base(t), tb, pbase, P);
-            else init_words<kTileWords, false>(S.ring, ring_base(t), tb, pbase, P);
+            if (t < ti0 || t >= ti1) init_words<kTileWords, true>(S.ring, at, tb, pbase, P);
+            else init_words<kTileWords, false>(S.ring, at, tb, pbase, P);
             pbase += kTileWords;
             if (pbase >= kPatWords) pbase -= kPatWords;
         };
@@ -576,19 +576,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         if (!waited) grid_dependency_wait();
         waited = true;
         // prologue: start t0; sieve t0 and start t0 + 1
-        start_tile(t0);
+        start_tile(t0, ring_base(t0));
         __syncthreads();
         scatter_medium(L, ring_addr + 4 * ring_base(t0), kTile);
         scatter_bucket(ring_addr + 4 * ring_base(t0), P, t0, 0);
-        if (t0 + 1 < t1) start_tile(t0 + 1);
+        if (t0 + 1 < t1) start_tile(t0 + 1, ring_base(t0 + 1));
         __syncthreads();
 
         // One phase per tile t, one barrier: scan t (reads t and the tail of
         // t - 1), finish t - 1's deferred words (t - 1, t - 2), sieve t + 1
         // (started last phase), start t + 2 -- five ring buffers, disjoint.
+        // ring bases of tiles t, t + 1, t + 2, advanced by one buffer per tile
+        uint32_t hb = ring_base(t0), hb1 = ring_base(t0 + 1), hb2 = ring_base(t0 + 2);
         for (uint32_t t = t0; t < t1; ++t) {
             const uint64_t tb = (uint64_t)t * kTile;
-            const uint32_t hb = ring_base(t);
             const bool edge = t < ti0 || t >= ti1;
             if (!FUSED) {
 #pragma unroll
@@ -627,14 +628,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                 if (KMAIN == 5 && t > t0) drain_residue(S, P, t - 1, need);
             }
             if (t + 1 < t1) {
-                const uint32_t hb1 = ring_base(t + 1);
 #ifndef SQF2K_EXP_NO_SCATTER
                 scatter_medium(L, ring_addr + 4 * hb1, kTile);
                 scatter_bucket(ring_addr + 4 * hb1, P, t + 1, 0);
 #endif
-                if (t + 2 < t1) start_tile(t + 2);
+                if (t + 2 < t1) start_tile(t + 2, hb2);
             }
             __syncthreads();
+            hb = hb1;
+            hb1 = hb2;
+            hb2 = hb2 + kTileWords == kRingWords ? 0u : hb2 + kTileWords;
             TLT(t - t0);
         }
         if (FUSED) {  // the chunk's last tile: deferred words and minima
