@@ -150,7 +150,7 @@ struct TileSmem {
     unsigned long long first[kDepthMax + 1];
     uint32_t first_t[2][6];       // k <= 5: least tile-local slot of tile t (buffer t & 1)
     uint32_t need;                // bit k: least n with exponent k still unknown
-    uint32_t cnt[kDepthMax + 1];  // counts of k >= 6 (rare)
+    uint32_t cnt[kDepthMax + 1];  // counts of k > kMainMax (rare)
     // words left after the main passes of tile t (queue t & 1), finished
     // while tile t + 1 is scanned
     uint32_t res_w[2][kResCap], res_p[2][kResCap];
@@ -299,11 +299,13 @@ __device__ __noinline__ void spill_word(uint32_t pend, uint64_t u0, int64_t base
         append(list, count, cap, (uint64_t)(base_n + 2 * (int64_t)(u0 + __ffs(x) - 1)));
 }
 
-// Passes k = 6..k_eff for one word (divergent, rare: ~0.02% of words).
+// Passes k = kMainMax+1..k_eff for one word (divergent, rare: ~0.02% of
+// words after 5 main passes).
 __device__ __forceinline__ void scan_residue(TileSmem &S, const TileParams &P, uint32_t hb,
                                              uint32_t w, uint64_t u0, uint32_t pend, uint32_t need) {
-    for (uint32_t k = 6; k <= P.k_eff && pend; ++k) {
-        const uint32_t sl = S.ring[ring_back(hb + w, 1u << (k - 6))];
+    for (uint32_t k = kMainMax + 1; k <= P.k_eff && pend; ++k) {
+        const uint32_t sl = k == 5 ? __funnelshift_l(S.ring[ring_back(hb + w, 1u)], S.ring[hb + w], 16)
+                                   : S.ring[ring_back(hb + w, 1u << (k - 6))];
         const uint32_t nw = pend & sl;
         if (nw) {
             atomicAdd(&S.cnt[k], (uint32_t)__popc(nw));
@@ -391,7 +393,7 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
             for (int i = 0; i < 4; ++i) {
                 if (!left[i]) continue;
                 const uint64_t u0 = tb + 32ull * (w0 + i);
-                if (KMAIN == 5) {
+                if (KMAIN == kMainMax) {
                     const uint32_t e = atomicAdd(&S.n_res[qi], 1u);
                     if (e < (uint32_t)kResCap) {  // deferred to the next tile's scan phase
                         S.res_w[qi][e] = w0 + i;
@@ -399,7 +401,7 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
                     } else {
                         scan_residue(S, P, hb, w0 + i, u0, left[i], need);
                     }
-                } else if (P.k_max > P.k_eff) {  // k_eff = KMAIN < 5: leftovers leave the tile
+                } else if (P.k_max > P.k_eff) {  // k_eff = KMAIN < kMainMax: leftovers leave the tile
                     spill_word(left[i], u0, P.base_n, P.esc, P.esc_count, P.esc_cap);
                 } else {
                     spill_word(left[i], u0, P.base_n, P.fail, P.fail_count, P.fail_cap);
@@ -625,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                     else scan_tile<false, false, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
                 }
 #endif
-                if (KMAIN == 5 && t > t0) drain_residue(S, P, t - 1, need);
+                if (KMAIN == kMainMax && t > t0) drain_residue(S, P, t - 1, need);
             }
             if (t + 1 < t1) {
 #ifndef SQF2K_EXP_NO_SCATTER
@@ -641,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             TLT(t - t0);
         }
         if (FUSED) {  // the chunk's last tile: deferred words and minima
-            if (KMAIN == 5) drain_residue(S, P, t1 - 1, S.need);
+            if (KMAIN == kMainMax) drain_residue(S, P, t1 - 1, S.need);
             const uint32_t ql = (t1 - 1) & 1u;
             if (threadIdx.x >= 1 && threadIdx.x <= 5 && S.first_t[ql][threadIdx.x] != ~0u) {
                 const unsigned long long f = (uint64_t)(t1 - 1) * kTile + S.first_t[ql][threadIdx.x];
@@ -668,7 +670,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         }
         const unsigned long long sc = __reduce_add_sync(0xffffffffu, scanned);
         if (lane == 0 && sc) atomicAdd(P.scanned, sc);
-        if (threadIdx.x >= 6 && threadIdx.x <= kDepthMax && S.cnt[threadIdx.x])
+        if (threadIdx.x > kMainMax && threadIdx.x <= kDepthMax && S.cnt[threadIdx.x])
             atomicAdd(&P.hist[threadIdx.x], (unsigned long long)S.cnt[threadIdx.x]);
     }
     // the last CTA resets the scheduler for the next launch and (single-batch
@@ -905,7 +907,7 @@ void run_tile_batch(const BatchArgs &a) {
     if (const char *g = std::getenv("SQF2K_DEBUG_GRID")) grid_cap = std::max(1, atoi(g));
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(n_tiles, grid_cap));
     if (a.fused) {
-        const uint32_t kmain = std::min<uint32_t>(a.k_eff, 5);
+        const uint32_t kmain = std::min<uint32_t>(a.k_eff, kMainMax);
         if (kmain == 1) launch_tile<true, 1>("tile_fused", grid, smem, P);
         else if (kmain == 2) launch_tile<true, 2>("tile_fused", grid, smem, P);
         else if (kmain == 3) launch_tile<true, 3>("tile_fused", grid, smem, P);

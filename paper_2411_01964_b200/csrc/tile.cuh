@@ -49,6 +49,11 @@ constexpr int kThreads = kTileWords / kWordsPerThread;  // CTA size
 #endif
 constexpr int kCtasPerSm = SQF2K_CTAS_PER_SM;
 constexpr int kDepthMax = 16;           // max exponent resolved in-tile
+#ifndef SQF2K_KMAIN_MAX
+#define SQF2K_KMAIN_MAX 5
+#endif
+constexpr int kMainMax = SQF2K_KMAIN_MAX;  // unconditional scan passes (4 or 5)
+static_assert(kMainMax == 4 || kMainMax == 5, "main passes");
 #ifndef SQF2K_DEPTH_DEFAULT
 #define SQF2K_DEPTH_DEFAULT 16
 #endif
