@@ -838,7 +838,20 @@ void run_tile_batch(const BatchArgs &a) {
 
     // bucket lists (sizes bounded on the host: no sync)
     uint32_t *counts = c.tile_counts.as<uint32_t>();
-    const unsigned bgrid = (unsigned)c.sm_count * 8;
+    // bucket work units (upper bound from pi(2^m) and the table size): no more
+    // CTAs than there is work for
+    uint64_t n_work = 0;
+    {
+        static const uint32_t pi2[kClasses + 1] = SQF2K_PI_POW2;
+        for (int j = 0; j < kClasses; ++j) {
+            const uint64_t hi = std::min<uint64_t>(pi2[j + 1], a.n_primes_bound);
+            if (hi <= pi2[j]) break;
+            const int sh = std::min(22 + 2 * j, 62);
+            n_work += (hi - pi2[j]) * ((a.U + (1ull << sh) - 1) >> sh);
+        }
+    }
+    const unsigned bgrid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>(ceil_div(n_work, 256), (uint64_t)c.sm_count * 8));
     const uint32_t *tile_start = nullptr;
     if (!a.exact_buckets) {
         c.hits.reserve((size_t)n_bt * kBucketCap * 2 + 64);
