@@ -181,6 +181,9 @@ __device__ __forceinline__ uint32_t smem_addr(const void *p) {
 // q = p^2).  o[j] is the lane's next hit relative to the current run of
 // slots; after clearing the hits in [0, len) it is rebased by -len, which
 // is exactly the next run's offset -- the offsets never leave registers.
+#ifndef SQF2K_SCATTER_UNROLL
+#define SQF2K_SCATTER_UNROLL 4
+#endif
 struct MedLane {
     uint32_t o[kTaskSlots], step[kTaskSlots];
 };
@@ -190,6 +193,14 @@ __device__ __forceinline__ void scatter_medium(MedLane &L, uint32_t wbase, uint3
     for (int j = 0; j < kTaskSlots; ++j) {
         const uint32_t st = L.step[j];
         uint32_t o = L.o[j];
+#if SQF2K_SCATTER_UNROLL == 4
+        for (; o + 3 * st < len; o += 4 * st) {
+            clear_bit(wbase, o);
+            clear_bit(wbase, o + st);
+            clear_bit(wbase, o + 2 * st);
+            clear_bit(wbase, o + 3 * st);
+        }
+#endif
         for (; o + st < len; o += 2 * st) {
             clear_bit(wbase, o);
             clear_bit(wbase, o + st);

@@ -68,7 +68,10 @@ constexpr int kMaxMed = 176;            // pi(1023) - 4 = 168
 #define SQF2K_TASK_SLOTS 2
 #endif
 constexpr int kTaskSlots = SQF2K_TASK_SLOTS;  // 32-lane scatter tasks per warp (registers)
-constexpr int kItemHits = 4;            // target hits per lane per tile
+#ifndef SQF2K_ITEM_HITS
+#define SQF2K_ITEM_HITS 4
+#endif
+constexpr int kItemHits = SQF2K_ITEM_HITS;  // target hits per lane per tile (medium schedule)
 #ifndef SQF2K_PATTERN_11
 #define SQF2K_PATTERN_11 0
 #endif
