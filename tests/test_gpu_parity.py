@@ -377,3 +377,17 @@ def test_dynamic_chunks_against_oracle(monkeypatch, grid):
                 got = verify_range(lo, hi, 30, pipeline=pipeline)
                 assert got.histogram == want["histogram"], (lo, grid, pipeline)
                 assert got.record_candidates == want["record_candidates"]
+
+
+def test_top_of_domain_window():
+    # the last odd n below 2^62 (the C ABI's domain end): primes up to 2^31,
+    # every bucket class, products near 2^62 in u64
+    hi = (1 << 62) - 1
+    lo = hi - 2 * 600_000
+    want = O.verify(lo, hi, width=1 << 30, k_max=30)
+    for pipeline in ("fused", "bitmap"):
+        got = verify_range(lo, hi, 30, pipeline=pipeline)
+        assert got.histogram == want["histogram"], pipeline
+        assert got.k_sum == want["k_sum"]
+        assert got.record_candidates == want["record_candidates"]
+        assert got.failures == want["failures"]
