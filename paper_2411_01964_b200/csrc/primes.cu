@@ -98,6 +98,7 @@ __device__ __forceinline__ uint32_t small_word(const SmallTables &T, uint32_t w,
 __global__ void __launch_bounds__(kSmallThreads) prime_small_kernel(uint64_t limit,
                                                                      uint32_t *__restrict__ out,
                                                                      PrimeInfo *__restrict__ info) {
+    grid_dependents_launch();  // the bucket fill may launch now (it waits for this grid)
     extern __shared__ uint32_t stage[];  // kSmallStage primes
     // the constant tables go to shared memory in one parallel round trip (a
     // cold constant cache would serialise one miss per line inside the loop)

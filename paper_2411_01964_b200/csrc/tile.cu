@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(256) bucket_kernel(
     uint64_t U, uint32_t *__restrict__ counts, const uint32_t *__restrict__ offsets,
     uint16_t *__restrict__ hits, unsigned int *__restrict__ overflow) {
     grid_dependents_launch();  // the tile kernel may start its prime-free prologue
+    grid_dependency_wait();    // launched early (PDL) behind the prime table: wait for it
     static_assert(kClasses <= 32, "one lane per class");
     __shared__ unsigned long long s_end[kClasses];  // cumulative work per class
     __shared__ uint32_t s_lo[kClasses];
@@ -866,9 +867,9 @@ void run_tile_batch(const BatchArgs &a) {
     const uint32_t *tile_start = nullptr;
     if (!a.exact_buckets) {
         c.hits.reserve((size_t)n_bt * kBucketCap * 2 + 64);
-        launch("bucket_fill", bucket_kernel<0>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
-               a.base_n, a.U, counts, (const uint32_t *)nullptr, c.hits.as<uint16_t>(),
-               a.overflow);
+        launch_pdl("bucket_fill", bucket_kernel<0>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
+                   a.base_n, a.U, counts, (const uint32_t *)nullptr, c.hits.as<uint16_t>(),
+                   a.overflow);
     } else {
         c.tile_offsets.reserve((n_bt + 1) * 4);
         uint32_t *offsets = c.tile_offsets.as<uint32_t>();
