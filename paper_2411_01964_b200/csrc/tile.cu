@@ -182,6 +182,11 @@ __device__ __forceinline__ uint32_t smem_addr(const void *p) {
 // q = p^2).  o[j] is the lane's next hit relative to the current run of
 // slots; after clearing the hits in [0, len) it is rebased by -len, which
 // is exactly the next run's offset -- the offsets never leave registers.
+#ifndef SQF2K_LPT_BUCKET
+#define SQF2K_LPT_BUCKET 4.0
+#define SQF2K_LPT_PER_TRIP 2.0
+#define SQF2K_LPT_TASK 2.0
+#endif
 #ifndef SQF2K_SCATTER_UNROLL
 #define SQF2K_SCATTER_UNROLL 4
 #endif
@@ -747,14 +752,15 @@ MedTables build_med(const std::vector<uint32_t> &med_primes) {
         const uint32_t n_tasks = (uint32_t)((descs.size() + 31) / 32);
         if (n_tasks > (uint32_t)(kWarps * kTaskSlots)) continue;
         std::vector<double> load(kWarps, 0.0);
-        load[kWarps - 1] = 4.0;  // the bucket warp (scatter_bucket)
+        load[kWarps - 1] = SQF2K_LPT_BUCKET;  // the bucket warp (scatter_bucket)
         std::vector<int> used(kWarps, 0);
         t.tasks.assign((size_t)kWarps * kTaskSlots * 64, 0u);  // step 0: idle lane
         for (uint32_t k = 0; k < n_tasks; ++k) {  // longest first, least-loaded warp with room
             int w = -1;
             for (int i = 0; i < kWarps; ++i)
                 if (used[i] < kTaskSlots && (w < 0 || load[i] < load[w])) w = i;
-            load[w] += descs[32 * k].trips / 2.0 + 2.0;  // two clears per trip + task overhead
+            // cost of a task: its longest lane (loop of 4 clears per trip) + overhead
+            load[w] += descs[32 * k].trips / SQF2K_LPT_PER_TRIP + SQF2K_LPT_TASK;
             const size_t at = ((size_t)w * kTaskSlots + used[w]++) * 64;
             for (uint32_t l = 0; l < 32; ++l) {
                 const uint32_t i = 32 * k + l;
