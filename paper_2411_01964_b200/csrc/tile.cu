@@ -139,7 +139,12 @@ __global__ void __launch_bounds__(256) bucket_kernel(
 // their hits with shared-memory atomics (random scatter: bank-conflict bound
 // at ~9 lanes/cycle/SM on B200, the same rate as byte stores, so no byte
 // array and no pack pass).
-constexpr int kRingTiles = 5;  // tiles t-2 .. t+2 are live in one phase
+#ifndef SQF2K_SPLIT_PHASE
+#define SQF2K_SPLIT_PHASE 0
+#endif
+// live tiles per phase: t-2 .. t+2 (5), or t-3 .. t+2 with the split phase
+// (tiles started 3 ahead, warps up to one phase apart) -- see tile_kernel
+constexpr int kRingTiles = SQF2K_SPLIT_PHASE ? 6 : 5;
 constexpr int kRingWords = kRingTiles * kTileWords;
 __device__ __forceinline__ uint32_t ring_base(uint32_t t) { return (t % kRingTiles) * kTileWords; }
 // ring word i - d (d <= kTileWords), wrapping below 0
@@ -156,6 +161,7 @@ struct TileSmem {
     // while tile t + 1 is scanned
     uint32_t res_w[2][kResCap], res_p[2][kResCap];
     uint32_t n_res[2];
+    unsigned long long mbar;  // split phase: one arrival per thread per phase
     uint32_t last;      // this CTA finished last (epilogue)
     uint32_t chunk[2];  // the dynamic chunk just taken
 };
@@ -176,6 +182,27 @@ __device__ __forceinline__ void clear_bit(uint32_t wbase, uint32_t o) {
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
+
+#if SQF2K_SPLIT_PHASE
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+}
+#endif
+
 
 // Medium primes 11 <= p < kPMed.  Each lane owns kTaskSlots descriptors
 // (host-balanced, see build_med): a start hit and a step (a multiple of
@@ -545,6 +572,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
     uint32_t scanned = 0;  // <= 128 per tile, < 2^21 tiles
     bool waited = false;
+#if SQF2K_SPLIT_PHASE
+    uint32_t mbar_phase = 0;  // phases this thread arrived on
+    if (threadIdx.x == 0) mbar_init(&S.mbar, kThreads);
+    __syncthreads();
+#endif
 
     for (;;) {
         if (t0 >= t1) {  // next dynamic chunk: one atomic, chunk index -> tiles
@@ -594,20 +626,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         TL(1);
         if (!waited) grid_dependency_wait();
         waited = true;
-        // prologue: start t0; sieve t0 and start t0 + 1
-        start_tile(t0, ring_base(t0));
-        __syncthreads();
-        scatter_medium(L, ring_addr + 4 * ring_base(t0), kTile);
-        scatter_bucket(ring_addr + 4 * ring_base(t0), P, t0, 0);
-        if (t0 + 1 < t1) start_tile(t0 + 1, ring_base(t0 + 1));
-        __syncthreads();
-
-        // One phase per tile t, one barrier: scan t (reads t and the tail of
-        // t - 1), finish t - 1's deferred words (t - 1, t - 2), sieve t + 1
-        // (started last phase), start t + 2 -- five ring buffers, disjoint.
-        // ring bases of tiles t, t + 1, t + 2, advanced by one buffer per tile
-        uint32_t hb = ring_base(t0), hb1 = ring_base(t0 + 1), hb2 = ring_base(t0 + 2);
-        for (uint32_t t = t0; t < t1; ++t) {
+        // Y work of tile t: scan (or store) it, finish t - 1's deferred words
+        auto scan_phase = [&](uint32_t t, uint32_t hb) {
             const uint64_t tb = (uint64_t)t * kTile;
             const bool edge = t < ti0 || t >= ti1;
             if (!FUSED) {
@@ -617,48 +637,98 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                     const uint4 v = *reinterpret_cast<const uint4 *>(&S.ring[hb + w]);
                     *reinterpret_cast<uint4 *>(&P.bits_out[(uint64_t)t * kTileWords + w]) = v;
                 }
-            } else {
-                // S.first[k] keeps this CTA's least slot with exponent k (its
-                // tiles come in increasing order and residue words finish in
-                // tile order); stop tracking a k once it is known (warp 0 folds
-                // tile t - 1's scan minima into S.first and clears S.need bits
-                // in this phase: a stale read only tracks once more).
-                const uint32_t need = S.need;
-                if (threadIdx.x < 32) {  // bookkeeping: warp 0 only (uniform branch)
-                    const uint32_t k = threadIdx.x, qp = (t + 1) & 1u;
-                    if (k >= 1 && k <= 5 && S.first_t[qp][k] != ~0u) {
-                        const unsigned long long f = tb - kTile + S.first_t[qp][k];
-                        if (f < S.first[k]) S.first[k] = f;
-                        S.first_t[qp][k] = ~0u;
-                    }
-                    const uint32_t known =
-                        __ballot_sync(0xffffffffu, k >= 1 && k <= kDepthMax && S.first[k] != ~0ull);
-                    if (k == 0) S.need &= ~known;
-                }
-#ifndef SQF2K_EXP_NO_SCAN
-                if (need & 0x3eu) {
-                    if (edge) scan_tile<true, true, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
-                    else scan_tile<false, true, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
-                } else {
-                    if (edge) scan_tile<true, false, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
-                    else scan_tile<false, false, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
-                }
-#endif
-                if (KMAIN == kMainMax && t > t0) drain_residue(S, P, t - 1, need);
+                return;
             }
-            if (t + 1 < t1) {
-#ifndef SQF2K_EXP_NO_SCATTER
-                scatter_medium(L, ring_addr + 4 * hb1, kTile);
-                scatter_bucket(ring_addr + 4 * hb1, P, t + 1, 0);
+            // S.first[k] keeps this CTA's least slot with exponent k (its
+            // tiles come in increasing order and residue words finish in
+            // tile order); stop tracking a k once it is known (warp 0 folds
+            // tile t - 1's scan minima into S.first and clears S.need bits
+            // in this phase: a stale read only tracks once more).
+            const uint32_t need = S.need;
+            if (threadIdx.x < 32) {  // bookkeeping: warp 0 only (uniform branch)
+                const uint32_t k = threadIdx.x, qp = (t + 1) & 1u;
+                if (k >= 1 && k <= 5 && S.first_t[qp][k] != ~0u) {
+                    const unsigned long long f = tb - kTile + S.first_t[qp][k];
+                    if (f < S.first[k]) S.first[k] = f;
+                    S.first_t[qp][k] = ~0u;
+                }
+                const uint32_t known =
+                    __ballot_sync(0xffffffffu, k >= 1 && k <= kDepthMax && S.first[k] != ~0ull);
+                if (k == 0) S.need &= ~known;
+            }
+#ifndef SQF2K_EXP_NO_SCAN
+            if (need & 0x3eu) {
+                if (edge) scan_tile<true, true, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+                else scan_tile<false, true, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+            } else {
+                if (edge) scan_tile<true, false, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+                else scan_tile<false, false, KMAIN>(S, P, hb, tb, need, c, scanned, t & 1u);
+            }
 #endif
+            if (KMAIN == kMainMax && t > t0) drain_residue(S, P, t - 1, need);
+        };
+        auto sieve_tile = [&](uint32_t t, uint32_t hb) {
+#ifndef SQF2K_EXP_NO_SCATTER
+            scatter_medium(L, ring_addr + 4 * hb, kTile);
+            scatter_bucket(ring_addr + 4 * hb, P, t, 0);
+#endif
+        };
+        auto next_base = [](uint32_t h) { return h + kTileWords == kRingWords ? 0u : h + kTileWords; };
+
+#if !SQF2K_SPLIT_PHASE
+        // prologue: start t0; sieve t0 and start t0 + 1
+        start_tile(t0, ring_base(t0));
+        __syncthreads();
+        sieve_tile(t0, ring_base(t0));
+        if (t0 + 1 < t1) start_tile(t0 + 1, ring_base(t0 + 1));
+        __syncthreads();
+
+        // One phase per tile t, one barrier: scan t (reads t and the tail of
+        // t - 1), finish t - 1's deferred words (t - 1, t - 2), sieve t + 1
+        // (started last phase), start t + 2 -- five ring buffers, disjoint.
+        // ring bases of tiles t, t + 1, t + 2, advanced by one buffer per tile
+        uint32_t hb = ring_base(t0), hb1 = ring_base(t0 + 1), hb2 = ring_base(t0 + 2);
+        for (uint32_t t = t0; t < t1; ++t) {
+            scan_phase(t, hb);
+            if (t + 1 < t1) {
+                sieve_tile(t + 1, hb1);
                 if (t + 2 < t1) start_tile(t + 2, hb2);
             }
             __syncthreads();
             hb = hb1;
             hb1 = hb2;
-            hb2 = hb2 + kTileWords == kRingWords ? 0u : hb2 + kTileWords;
+            hb2 = next_base(hb2);
             TLT(t - t0);
         }
+#else
+        // prologue: start t0 .. t0 + 2; sieve t0
+        start_tile(t0, ring_base(t0));
+        if (t0 + 1 < t1) start_tile(t0 + 1, ring_base(t0 + 1));
+        if (t0 + 2 < t1) start_tile(t0 + 2, ring_base(t0 + 2));
+        __syncthreads();
+        sieve_tile(t0, ring_base(t0));
+        __syncthreads();
+
+        // Split phase per tile t: sieve t + 1 (started 2 phases ago), then
+        // wait for the previous phase, start t + 3, scan t, finish t - 1's
+        // deferred words, arrive.  The uneven sieve work of a warp overlaps
+        // the others finishing the previous phase; warps are at most one
+        // phase apart, so six ring buffers (t - 3 .. t + 2) stay disjoint.
+        uint32_t hb = ring_base(t0), hb1 = ring_base(t0 + 1), hb3 = ring_base(t0 + 3);
+        for (uint32_t t = t0; t < t1; ++t) {
+            if (t + 1 < t1) sieve_tile(t + 1, hb1);
+            if (t > t0) mbar_wait(&S.mbar, (mbar_phase - 1) & 1u);
+            if (t + 3 < t1) start_tile(t + 3, hb3);
+            scan_phase(t, hb);
+            mbar_arrive(&S.mbar);
+            ++mbar_phase;
+            hb = hb1;
+            hb1 = next_base(hb1);
+            hb3 = next_base(hb3);
+            TLT(t - t0);
+        }
+        mbar_wait(&S.mbar, (mbar_phase - 1) & 1u);
+#endif
         if (FUSED) {  // the chunk's last tile: deferred words and minima
             if (KMAIN == kMainMax) drain_residue(S, P, t1 - 1, S.need);
             const uint32_t ql = (t1 - 1) & 1u;
