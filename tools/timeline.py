@@ -71,3 +71,5 @@ for sm, ids in ranks.items():
 print("group sizes", sorted(set(len(v) for v in ranks.values())))
 print("loop by start-rank on SM:", [round(float(np.mean(x)), 1) for x in by_rank if x])
 print("loop by blockIdx-rank on SM:", [round(float(np.mean(x)), 1) for x in by_bidx if x])
+print("loop by blockIdx % 4:", [round(float(loop[np.arange(g) % 4 == j].mean()), 1) for j in range(4)])
+print("loop by blockIdx % 4 (std):", [round(float(loop[np.arange(g) % 4 == j].std()), 1) for j in range(4)])
