@@ -209,6 +209,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t pari
 // q = p^2).  o[j] is the lane's next hit relative to the current run of
 // slots; after clearing the hits in [0, len) it is rebased by -len, which
 // is exactly the next run's offset -- the offsets never leave registers.
+#ifndef SQF2K_SCAN_CHUNK
+#define SQF2K_SCAN_CHUNK 4
+#endif
 #ifndef SQF2K_LPT_BUCKET
 #define SQF2K_LPT_BUCKET 4.0
 #define SQF2K_LPT_PER_TRIP 2.0
@@ -406,16 +409,26 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
     const uint32_t wt = W * threadIdx.x;
     uint32_t f[6] = {~0u, ~0u, ~0u, ~0u, ~0u, ~0u};  // TRACK: least tile-local slot per k
     uint32_t prv_in = S.ring[hb + wt ? hb + wt - 1 : kRingWords - 1];
+    constexpr int CW = SQF2K_SCAN_CHUNK;  // words scanned together (ILP vs registers)
 #pragma unroll
-    for (int ch = 0; ch < W / 4; ++ch) {
-        const uint32_t w0 = wt + 4 * ch;
-        const uint4 cw = *reinterpret_cast<const uint4 *>(&S.ring[hb + w0]);
-        const uint32_t cur[4] = {cw.x, cw.y, cw.z, cw.w};
-        const uint32_t prv[4] = {prv_in, cw.x, cw.y, cw.z};
-        prv_in = cw.w;
-        uint32_t left[4], any = 0;
+    for (int ch = 0; ch < W / CW; ++ch) {
+        const uint32_t w0 = wt + CW * ch;
+        uint32_t cur[CW], prv[CW];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int v = 0; v < CW / 4; ++v) {
+            const uint4 cw = *reinterpret_cast<const uint4 *>(&S.ring[hb + w0 + 4 * v]);
+            cur[4 * v] = cw.x;
+            cur[4 * v + 1] = cw.y;
+            cur[4 * v + 2] = cw.z;
+            cur[4 * v + 3] = cw.w;
+        }
+        prv[0] = prv_in;
+#pragma unroll
+        for (int i = 1; i < CW; ++i) prv[i] = cur[i - 1];
+        prv_in = cur[CW - 1];
+        uint32_t left[CW], any = 0;
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
             const uint64_t u0 = tb + 32ull * (w0 + i);
             uint32_t pend = ~0u;
             if (EDGE) {
@@ -431,10 +444,10 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
             left[i] = scan_word<TRACK, KMAIN>(pend, prv[i], cur[i], c, f, w0 + i);
             any |= left[i];
         }
-        if (!EDGE) scanned += 128;
+        if (!EDGE) scanned += 32 * CW;
         if (any) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < CW; ++i) {
                 if (!left[i]) continue;
                 const uint64_t u0 = tb + 32ull * (w0 + i);
                 if (KMAIN == kMainMax) {
