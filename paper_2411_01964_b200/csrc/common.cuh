@@ -68,6 +68,9 @@ struct Context {
     // captured into the same graph as parallel branches)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // multi-batch calls: batch b's bucket lists are built on the side stream
+    // (buffer set b & 1) while batch b - 1's tile kernel runs
+    cudaEvent_t ev_primes = nullptr, ev_prep = nullptr, ev_tile[2] = {nullptr, nullptr};
     std::recursive_mutex mu;
 
     // profiling: events recorded around launches, resolved lazily
@@ -85,6 +88,7 @@ struct Context {
     DevBuf residues, items, tile_counts, tile_offsets, hits;
     DevBuf acc, esc, fail, fail_sorted, window, kvals, bits_out, host_primes;
     DevBuf pattern, prime_info, sched;
+    DevBuf pattern_b, tile_counts_b, hits_b;  // second buffer set (batch parity 1)
     void *pinned = nullptr;  // small pinned host staging (summary readback)
     uint64_t h2d_bytes = 0, d2h_bytes = 0;  // copy accounting (bench e2e)
     uint64_t primes_limit = 0;  // primes_u32 holds all primes <= primes_limit

@@ -152,7 +152,11 @@ int sqf2k_init(int device) {
     }
     if ((e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming)) != cudaSuccess) {
+        (e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_primes, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_prep, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_tile[0], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_tile[1], cudaEventDisableTiming)) != cudaSuccess) {
         cudaStreamDestroy(c->stream);
         delete c;
         return fail(SQF2K_ECUDA, "side stream: %s", cudaGetErrorString(e));
@@ -176,7 +180,8 @@ void sqf2k_shutdown(void) {
                       &c->scan_tmp, &c->residues, &c->items, &c->tile_counts,
                       &c->tile_offsets, &c->hits, &c->acc, &c->esc,
                       &c->fail, &c->fail_sorted, &c->window, &c->kvals, &c->bits_out,
-                      &c->host_primes, &c->pattern, &c->prime_info, &c->sched})
+                      &c->host_primes, &c->pattern, &c->prime_info, &c->sched,
+                      &c->pattern_b, &c->tile_counts_b, &c->hits_b})
         b->release();
     if (c->pinned) cudaFreeHost(c->pinned);
     for (auto &p : c->pending) {
@@ -187,6 +192,7 @@ void sqf2k_shutdown(void) {
     cudaStreamSynchronize(c->side);
     cudaEventDestroy(c->ev_fork);
     cudaEventDestroy(c->ev_join);
+    for (cudaEvent_t ev : {c->ev_primes, c->ev_prep, c->ev_tile[0], c->ev_tile[1]}) cudaEventDestroy(ev);
     cudaStreamDestroy(c->side);
     cudaStreamDestroy(c->stream);
     delete c;

@@ -921,13 +921,43 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
     }
 
     // p = 3, 5, 7 pattern of this domain
-    c.pattern.reserve((kPatWords + kTileWords) * 4);
+    DevBuf &pattern = a.buf ? c.pattern_b : c.pattern;
+    DevBuf &counts = a.buf ? c.tile_counts_b : c.tile_counts;
+    pattern.reserve((kPatWords + kTileWords) * 4);
     launch_on(st, "pattern", pattern_kernel,
               dim3((unsigned)std::min<uint64_t>(ceil_div(kPatWords + kTileWords, 256), c.sm_count * 8)), dim3(256),
-              0, a.base_n, a.pattern_present, c.pattern.as<uint32_t>());
+              0, a.base_n, a.pattern_present, pattern.as<uint32_t>());
     const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);
-    c.tile_counts.reserve((n_bt + 1) * 4);
-    SQF2K_CUDA(cudaMemsetAsync(c.tile_counts.ptr, 0, (n_bt + 1) * 4, st));
+    counts.reserve((n_bt + 1) * 4);
+    SQF2K_CUDA(cudaMemsetAsync(counts.ptr, 0, (n_bt + 1) * 4, st));
+}
+
+// bucket work units (upper bound from pi(2^m) and the table size)
+static unsigned bucket_grid(const BatchArgs &a) {
+    uint64_t n_work = 0;
+    static const uint32_t pi2[kClasses + 1] = SQF2K_PI_POW2;
+    for (int j = 0; j < kClasses; ++j) {
+        const uint64_t hi = std::min<uint64_t>(pi2[j + 1], a.n_primes_bound);
+        if (hi <= pi2[j]) break;
+        const int sh = std::min(22 + 2 * j, 62);
+        n_work += (hi - pi2[j]) * ((a.U + (1ull << sh) - 1) >> sh);
+    }
+    return (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>(ceil_div(n_work, 256), (uint64_t)ctx().sm_count * 8));
+}
+
+// Fixed-capacity bucket lists of a batch on stream st (after its prep and
+// the prime table): lets a multi-batch call build batch b's lists while
+// batch b - 1's tile kernel runs.
+void bucket_batch(const BatchArgs &a, cudaStream_t st) {
+    Context &c = ctx();
+    const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);
+    DevBuf &hits = a.buf ? c.hits_b : c.hits;
+    DevBuf &counts = a.buf ? c.tile_counts_b : c.tile_counts;
+    hits.reserve((size_t)n_bt * kBucketCap * 2 + 64);
+    launch_on(st, "bucket_fill", bucket_kernel<0>, dim3(bucket_grid(a)), dim3(256), 0, a.primes,
+              a.info, a.base_n, a.U, counts.as<uint32_t>(), (const uint32_t *)nullptr,
+              hits.as<uint16_t>(), a.overflow);
 }
 
 // Bucket lists and the tile kernel of a batch (after prep_tile_batch and the
@@ -938,31 +968,21 @@ void run_tile_batch(const BatchArgs &a) {
     const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);
 
     // bucket lists (sizes bounded on the host: no sync)
-    uint32_t *counts = c.tile_counts.as<uint32_t>();
-    // bucket work units (upper bound from pi(2^m) and the table size): no more
-    // CTAs than there is work for
-    uint64_t n_work = 0;
-    {
-        static const uint32_t pi2[kClasses + 1] = SQF2K_PI_POW2;
-        for (int j = 0; j < kClasses; ++j) {
-            const uint64_t hi = std::min<uint64_t>(pi2[j + 1], a.n_primes_bound);
-            if (hi <= pi2[j]) break;
-            const int sh = std::min(22 + 2 * j, 62);
-            n_work += (hi - pi2[j]) * ((a.U + (1ull << sh) - 1) >> sh);
-        }
-    }
-    const unsigned bgrid = (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>(ceil_div(n_work, 256), (uint64_t)c.sm_count * 8));
+    DevBuf &hits = a.buf ? c.hits_b : c.hits;
+    uint32_t *counts = (a.buf ? c.tile_counts_b : c.tile_counts).as<uint32_t>();
+    const unsigned bgrid = bucket_grid(a);
     const uint32_t *tile_start = nullptr;
-    if (!a.exact_buckets) {
-        c.hits.reserve((size_t)n_bt * kBucketCap * 2 + 64);
+    if (a.bucket_stream) {
+        // lists already built by bucket_batch
+    } else if (!a.exact_buckets) {
+        hits.reserve((size_t)n_bt * kBucketCap * 2 + 64);
         launch_pdl("bucket_fill", bucket_kernel<0>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
-                   a.base_n, a.U, counts, (const uint32_t *)nullptr, c.hits.as<uint16_t>(),
+                   a.base_n, a.U, counts, (const uint32_t *)nullptr, hits.as<uint16_t>(),
                    a.overflow);
     } else {
         c.tile_offsets.reserve((n_bt + 1) * 4);
         uint32_t *offsets = c.tile_offsets.as<uint32_t>();
-        c.hits.reserve(bucket_hits_bound(a.U, a.n_primes_bound) * 2 + 64);
+        hits.reserve(bucket_hits_bound(a.U, a.n_primes_bound) * 2 + 64);
         launch("bucket_count", bucket_kernel<1>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
                a.base_n, a.U, counts, (const uint32_t *)offsets, (uint16_t *)nullptr, a.overflow);
         size_t tmp_bytes = 0;
@@ -972,7 +992,7 @@ void run_tile_batch(const BatchArgs &a) {
         SQF2K_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.ptr, tmp_bytes, counts, offsets,
                                                  (int)n_bt + 1, c.stream));
         launch("bucket_fill", bucket_kernel<2>, dim3(bgrid), dim3(256), 0, a.primes, a.info,
-               a.base_n, a.U, counts, (const uint32_t *)offsets, c.hits.as<uint16_t>(),
+               a.base_n, a.U, counts, (const uint32_t *)offsets, hits.as<uint16_t>(),
                a.overflow);
         tile_start = offsets;
     }
@@ -990,12 +1010,12 @@ void run_tile_batch(const BatchArgs &a) {
     P.k_eff = a.k_eff;
     P.k_max = a.k_max;
 
-    P.pattern = c.pattern.as<uint32_t>();
+    P.pattern = (a.buf ? c.pattern_b : c.pattern).as<uint32_t>();
     P.med = g_med.buf.as<uint32_t>();
     P.tasks = reinterpret_cast<const uint2 *>(g_med.buf.as<uint32_t>() + kMaxMed);
     P.tile_start = tile_start;
     P.tile_count = counts;
-    P.hits = c.hits.as<uint16_t>();
+    P.hits = hits.as<uint16_t>();
     P.hist = a.hist;
     P.min_n = a.min_n;
     P.esc = a.esc;

@@ -182,10 +182,14 @@ struct BatchArgs {
     uint32_t *bits_out;
     bool exact_buckets;           // count + scan + fill instead of fixed capacity
     unsigned int *overflow;       // set when a fixed-capacity list overflowed
+    int buf;                      // buffer set (pattern, bucket lists): 0 or 1
+    cudaStream_t bucket_stream;   // non-null: run_tile_batch skips the (fixed) bucket fill,
+                                  //   done earlier by bucket_batch on that stream
     struct Acc *finish_acc;       // non-null: the tile kernel's last CTA finishes the call
     void *finish_host;            //   (escalation + accumulators to this mapped host buffer)
 };
 void prep_tile_batch(const BatchArgs &a, cudaStream_t st);
+void bucket_batch(const BatchArgs &a, cudaStream_t st);
 void run_tile_batch(const BatchArgs &a);
 
 }  // namespace sqf2k

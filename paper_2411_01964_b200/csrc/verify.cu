@@ -230,11 +230,33 @@ void enqueue_verify(const VerifyPlan &pl) {
     // the (rare) escalations and writes the accumulators to pinned memory
     const bool finish_in_tile = pl.pipeline == 0 && pl.n_slots <= pl.batch &&
                                 pl.k_eff >= (uint32_t)kDepthDefault;
-    for (uint64_t s0 = 0; s0 < pl.n_slots; s0 += pl.batch) {
+    // several fused batches with fixed-capacity lists: batch b's pattern and
+    // bucket lists are built on the side stream (buffer set b & 1) while batch
+    // b - 1's tile kernel runs on the main stream (its tail frees the SMs)
+    const bool overlap = pl.pipeline == 0 && !pl.exact && pl.n_slots > pl.batch;
+    if (overlap) SQF2K_CUDA(cudaEventRecord(c.ev_primes, c.stream));
+    uint64_t b = 0;
+    for (uint64_t s0 = 0; s0 < pl.n_slots; s0 += pl.batch, ++b) {
         const auto [A, sb] = set_batch(s0);
-        if (s0) prep_tile_batch(a, c.stream);
         a.finish_acc = finish_in_tile ? acc : nullptr;
         a.finish_host = c.pinned;
+        if (overlap) {
+            a.buf = (int)(b & 1);
+            a.bucket_stream = c.side;
+            if (b) {
+                if (b >= 2) SQF2K_CUDA(cudaStreamWaitEvent(c.side, c.ev_tile[b & 1], 0));
+                prep_tile_batch(a, c.side);  // buffer set b & 1 is free again
+            } else {
+                SQF2K_CUDA(cudaStreamWaitEvent(c.side, c.ev_primes, 0));
+            }
+            bucket_batch(a, c.side);
+            SQF2K_CUDA(cudaEventRecord(c.ev_prep, c.side));
+            SQF2K_CUDA(cudaStreamWaitEvent(c.stream, c.ev_prep, 0));
+            run_tile_batch(a);
+            SQF2K_CUDA(cudaEventRecord(c.ev_tile[b & 1], c.stream));
+            continue;
+        }
+        if (s0) prep_tile_batch(a, c.stream);
         run_tile_batch(a);
         if (pl.pipeline == 1)
             scan_bitmap_device(c.window.as<uint32_t>(), H / 32, sb, A, pl.k_eff, pl.k_max,
