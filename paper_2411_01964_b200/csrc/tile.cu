@@ -209,6 +209,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t pari
 // q = p^2).  o[j] is the lane's next hit relative to the current run of
 // slots; after clearing the hits in [0, len) it is rebased by -len, which
 // is exactly the next run's offset -- the offsets never leave registers.
+#ifndef SQF2K_TMA_EXPORT
+#define SQF2K_TMA_EXPORT 1
+#endif
 #ifndef SQF2K_SCAN_CHUNK
 #define SQF2K_SCAN_CHUNK 4
 #endif
@@ -644,12 +647,26 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             const uint64_t tb = (uint64_t)t * kTile;
             const bool edge = t < ti0 || t >= ti1;
             if (!FUSED) {
+#if SQF2K_TMA_EXPORT
+                // one bulk copy (TMA engine) of the sieved tile to HBM; the
+                // buffer is rewritten 3 phases later (wait_group.read below)
+                if (threadIdx.x == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    asm volatile(
+                        "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                            P.bits_out + (uint64_t)t * kTileWords),
+                        "r"(ring_addr + 4 * hb), "r"((uint32_t)kTileWords * 4)
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+#else
 #pragma unroll
                 for (int ch = 0; ch < kWordsPerThread / 4; ++ch) {
                     const uint32_t w = 4 * (threadIdx.x + ch * kThreads);
                     const uint4 v = *reinterpret_cast<const uint4 *>(&S.ring[hb + w]);
                     *reinterpret_cast<uint4 *>(&P.bits_out[(uint64_t)t * kTileWords + w]) = v;
                 }
+#endif
                 return;
             }
             // S.first[k] keeps this CTA's least slot with exponent k (its
@@ -707,12 +724,22 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                 sieve_tile(t + 1, hb1);
                 if (t + 2 < t1) start_tile(t + 2, hb2);
             }
+#if SQF2K_TMA_EXPORT
+            // next phase starts tile t + 3 in buffer t - 2: its store (group
+            // t - 2) must have read the buffer; t - 1 and t may stay in flight
+            if (!FUSED && threadIdx.x == 0)
+                asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+#endif
             __syncthreads();
             hb = hb1;
             hb1 = hb2;
             hb2 = next_base(hb2);
             TLT(t - t0);
         }
+#if SQF2K_TMA_EXPORT
+        // the next chunk restarts the ring: every store must have read its buffer
+        if (!FUSED && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
 #else
         // prologue: start t0 .. t0 + 2; sieve t0
         start_tile(t0, ring_base(t0));
@@ -755,6 +782,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     }
 
     TL(2);
+#if SQF2K_TMA_EXPORT
+    if (!FUSED && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
     if (FUSED) {  // this CTA's minima and counts
         __syncthreads();
         if (threadIdx.x >= 1 && threadIdx.x <= kDepthMax) {
