@@ -54,6 +54,9 @@ struct ScanParams {
 // derives it from `scanned` by conservation, as for the fused kernel.
 constexpr int kFastThreads = 256;
 constexpr int kGroupWords = 8;
+#ifndef SQF2K_TMA_SCAN
+#define SQF2K_TMA_SCAN 0
+#endif
 
 // Pending mask of the word starting at slot a (end of range, n = 1).
 __device__ __forceinline__ uint32_t wscan_mask(const ScanParams &P, uint64_t a) {
@@ -140,7 +143,7 @@ __device__ __forceinline__ void wscan_group(const ScanParams &P, const uint32_t 
 }
 
 // the group's words (2 x LDG.128); lanes hold consecutive groups
-__device__ __forceinline__ void wscan_load(const ScanParams &P, uint64_t wg,
+[[maybe_unused]] __device__ __forceinline__ void wscan_load(const ScanParams &P, uint64_t wg,
                                            uint32_t (&cur)[kGroupWords]) {
 #pragma unroll
     for (int v = 0; v < kGroupWords / 4; ++v) {
@@ -197,6 +200,113 @@ __global__ void __launch_bounds__(kFastThreads) wscan_kernel(const ScanParams P)
             else
                 wscan_group<KMAIN, false, false>(P, w, g, word0, cur, prv, c, scanned, tneed, s_cnt, s_first);
         }
+    }
+#pragma unroll
+    for (int k = 2; k <= 5; ++k) {
+        const uint32_t s = __reduce_add_sync(0xffffffffu, c[k]);
+        if ((threadIdx.x & 31) == 0 && s) atomicAdd(&s_cnt[k], s);
+    }
+    for (int d = 16; d >= 1; d >>= 1) scanned += __shfl_xor_sync(0xffffffffu, scanned, d);
+    if ((threadIdx.x & 31) == 0 && scanned) atomicAdd(P.scanned, scanned);
+    __syncthreads();
+    for (int k = threadIdx.x; k < 65; k += blockDim.x) {
+        if (s_cnt[k]) atomicAdd(&P.hist[k], (unsigned long long)s_cnt[k]);
+        if (s_first[k] != ~0ull)
+            atomicMin(&P.min_n[k], (unsigned long long)(P.first_n + 2 * s_first[k]));
+    }
+}
+
+// TMA-fed variant: the CTA's contiguous run of groups streams through a
+// kStages-deep ring of 8 KB shared-memory blocks, each filled by one bulk copy
+// (cp.async.bulk global -> shared, completion on an mbarrier) issued by thread
+// 0 kStages - 1 blocks ahead; threads read their group (2 x LDS.128) and the
+// word before it from shared memory.  No per-thread global loads on the path.
+constexpr int kStages = 4;
+constexpr int kBlockGroups = kFastThreads;                  // groups per block
+constexpr int kBlockWords = kBlockGroups * kGroupWords;     // 2048 words = 8 KB
+constexpr int kStageWords = kBlockWords + 4;                // + 16 B: the word before
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+template <int KMAIN>
+__global__ void __launch_bounds__(kFastThreads) wscan_tma_kernel(const ScanParams P) {
+    extern __shared__ __align__(128) uint32_t stage[];  // kStages x kStageWords
+    __shared__ __align__(8) unsigned long long full[kStages];
+    __shared__ unsigned long long s_first[65];
+    __shared__ uint32_t s_cnt[65];
+    for (int k = threadIdx.x; k < 65; k += blockDim.x) {
+        s_first[k] = ~0ull;
+        s_cnt[k] = 0;
+    }
+    if (threadIdx.x == 0)
+        for (int i = 0; i < kStages; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[i])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(P.w4);
+    const uint64_t word0 = P.c0 * 4;  // word index of slot 0 (a multiple of 4)
+    const uint64_t n_groups = (P.n_slots + 32 * kGroupWords - 1) / (32 * kGroupWords);
+    const uint64_t g_lo = n_groups * blockIdx.x / gridDim.x;
+    const uint64_t g_hi = n_groups * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t n_blocks = (g_hi - g_lo + kBlockGroups - 1) / kBlockGroups;
+    auto issue = [&](uint64_t j) {  // block j of this CTA into stage j % kStages
+        const uint64_t g0 = g_lo + j * kBlockGroups;
+        const uint64_t left_g = g_hi - g0;
+        const uint32_t ng = left_g < (uint64_t)kBlockGroups ? (uint32_t)left_g : (uint32_t)kBlockGroups;
+        const uint32_t bytes = (ng * kGroupWords + 4) * 4;
+        const uint32_t st = (uint32_t)(j % kStages);
+        const uint32_t bar = smem_u32(&full[st]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(stage + st * kStageWords)),
+            "l"(w + word0 + g0 * kGroupWords - 4), "r"(bytes), "r"(bar)
+            : "memory");
+    };
+    if (threadIdx.x == 0)
+        for (uint64_t j = 0; j < kStages - 1 && j < n_blocks; ++j) issue(j);
+    uint32_t c[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long scanned = 0;
+    uint32_t tneed = (2u << KMAIN) - 2u;  // k = 1..KMAIN not met yet by this thread
+    const uint64_t g_edge = P.n_slots / (32 * kGroupWords);  // groups >= this touch the end
+    const uint64_t g_one = P.one_slot == ~0ull ? ~0ull : P.one_slot / (32 * kGroupWords);
+    for (uint64_t j = 0; j < n_blocks; ++j) {
+        const uint32_t st = (uint32_t)(j % kStages);
+        if (threadIdx.x == 0 && j + kStages - 1 < n_blocks) issue(j + kStages - 1);
+        // wait for block j (phase parity of its stage)
+        const uint32_t parity = (uint32_t)((j / kStages) & 1);
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+                "selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(smem_u32(&full[st])), "r"(parity)
+                : "memory");
+        const uint64_t g = g_lo + j * kBlockGroups + threadIdx.x;
+        if (g < g_hi) {
+            const uint32_t *b = stage + st * kStageWords + 4 + threadIdx.x * kGroupWords;
+            uint32_t cur[kGroupWords];
+#pragma unroll
+            for (int v = 0; v < kGroupWords / 4; ++v) {
+                const uint4 x = *reinterpret_cast<const uint4 *>(b + 4 * v);
+                cur[4 * v] = x.x;
+                cur[4 * v + 1] = x.y;
+                cur[4 * v + 2] = x.z;
+                cur[4 * v + 3] = x.w;
+            }
+            const uint32_t prv = b[-1];
+            if (g >= g_edge || g == g_one)
+                wscan_group<KMAIN, true, true>(P, w, g, word0, cur, prv, c, scanned, tneed, s_cnt, s_first);
+            else if (tneed)
+                wscan_group<KMAIN, true, false>(P, w, g, word0, cur, prv, c, scanned, tneed, s_cnt, s_first);
+            else
+                wscan_group<KMAIN, false, false>(P, w, g, word0, cur, prv, c, scanned, tneed, s_cnt, s_first);
+        }
+        __syncthreads();  // stage st may be refilled (block j + kStages) from here on
     }
 #pragma unroll
     for (int k = 2; k <= 5; ++k) {
@@ -433,6 +543,23 @@ void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_sl
     const uint64_t groups = ceil_div(n_slots, 32 * kGroupWords);
     const unsigned grid = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>(ceil_div(groups, kFastThreads), (uint64_t)ctx().sm_count * 8));
+#if SQF2K_TMA_SCAN
+    const size_t smem = (size_t)kStages * kStageWords * 4;
+    static bool attr = false;
+    if (!attr) {
+        for (auto *k : {wscan_tma_kernel<1>, wscan_tma_kernel<2>, wscan_tma_kernel<3>,
+                        wscan_tma_kernel<4>, wscan_tma_kernel<5>})
+            SQF2K_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    switch (std::min<uint32_t>(k_scan, 5)) {
+        case 1: launch("window_scan", wscan_tma_kernel<1>, dim3(grid), dim3(kFastThreads), smem, P); break;
+        case 2: launch("window_scan", wscan_tma_kernel<2>, dim3(grid), dim3(kFastThreads), smem, P); break;
+        case 3: launch("window_scan", wscan_tma_kernel<3>, dim3(grid), dim3(kFastThreads), smem, P); break;
+        case 4: launch("window_scan", wscan_tma_kernel<4>, dim3(grid), dim3(kFastThreads), smem, P); break;
+        default: launch("window_scan", wscan_tma_kernel<5>, dim3(grid), dim3(kFastThreads), smem, P); break;
+    }
+#else
     switch (std::min<uint32_t>(k_scan, 5)) {
         case 1: launch("window_scan", wscan_kernel<1>, dim3(grid), dim3(kFastThreads), 0, P); break;
         case 2: launch("window_scan", wscan_kernel<2>, dim3(grid), dim3(kFastThreads), 0, P); break;
@@ -440,6 +567,7 @@ void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_sl
         case 4: launch("window_scan", wscan_kernel<4>, dim3(grid), dim3(kFastThreads), 0, P); break;
         default: launch("window_scan", wscan_kernel<5>, dim3(grid), dim3(kFastThreads), 0, P); break;
     }
+#endif
 }
 
 }  // namespace sqf2k
