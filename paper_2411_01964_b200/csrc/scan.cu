@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(kFastThreads) wscan_kernel(const ScanParams P)
     }
 }
 
+#if SQF2K_TMA_SCAN
 // TMA-fed variant: the CTA's contiguous run of groups streams through a
 // kStages-deep ring of 8 KB shared-memory blocks, each filled by one bulk copy
 // (cp.async.bulk global -> shared, completion on an mbarrier) issued by thread
@@ -322,6 +323,8 @@ __global__ void __launch_bounds__(kFastThreads) wscan_tma_kernel(const ScanParam
             atomicMin(&P.min_n[k], (unsigned long long)(P.first_n + 2 * s_first[k]));
     }
 }
+
+#endif  // SQF2K_TMA_SCAN
 
 template <bool EXPO>
 __global__ void __launch_bounds__(kScanThreads) window_scan_kernel(const ScanParams P) {
