@@ -16,6 +16,14 @@ namespace sqf2k {
 
 namespace {
 
+#ifndef SQF2K_TMA_START
+#define SQF2K_TMA_START 1
+#endif
+// tile starts by one bulk copy from the pattern table need 16-byte aligned
+// sources: four copies of the table, shifted by one word each
+constexpr uint32_t kPatCopies = SQF2K_TMA_START ? 4 : 1;
+constexpr uint32_t kPatStride = (kPatWords + kTileWords + 3) / 4 * 4;
+
 // -------------------------------------------------------------------------
 // p = 3, 5, 7 (11): word g of the domain (slots 32g..32g+31) with every slot
 // u such that 9, 25, 49 (or 121) divides n(u) cleared.  Period kPatWords
@@ -30,8 +38,11 @@ __global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__res
     uint32_t r[4];
 #pragma unroll
     for (int i = 0; i < NP; ++i) r[i] = (uint32_t)slot_residue(base_n, q[i]);
-    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < kPatWords + kTileWords;
-         g += gridDim.x * blockDim.x) {
+    // copy r (r = 0..kPatCopies-1) at table + r * kPatStride holds word g + r at
+    // index g, so a tile start at any pattern index has a 16-byte aligned source
+    for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < kPatCopies * kPatStride;
+         gi += gridDim.x * blockDim.x) {
+        const uint32_t g = gi % kPatStride + gi / kPatStride;
         uint32_t clr = 0;
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
@@ -39,7 +50,7 @@ __global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__res
             const uint32_t y = (r[i] + q[i] - (32u * g) % q[i]) % q[i];
             if (y < 32) clr |= pat[i] << y;
         }
-        table[g] = ~clr;
+        table[gi] = ~clr;
     }
 }
 
@@ -162,6 +173,7 @@ struct TileSmem {
     uint32_t res_w[2][kResCap], res_p[2][kResCap];
     uint32_t n_res[2];
     unsigned long long mbar;  // split phase: one arrival per thread per phase
+    unsigned long long mbar_start;  // TMA tile starts: one bulk copy per use
     uint32_t last;      // this CTA finished last (epilogue)
     uint32_t chunk[2];  // the dynamic chunk just taken
 };
@@ -588,6 +600,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
     uint32_t scanned = 0;  // <= 128 per tile, < 2^21 tiles
     bool waited = false;
+    constexpr bool kTmaStart = SQF2K_TMA_START && !SQF2K_SPLIT_PHASE;
+    bool start_pending = false;  // thread 0: a start's bulk copy is in flight
+    uint32_t start_parity = 0;
+    if (kTmaStart) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&S.mbar_start))
+                         : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
 #if SQF2K_SPLIT_PHASE
     uint32_t mbar_phase = 0;  // phases this thread arrived on
     if (threadIdx.x == 0) mbar_init(&S.mbar, kThreads);
@@ -617,10 +640,46 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         uint32_t pbase = (uint32_t)((b0 / 32) % kPatWords);  // pattern index of the next start
         auto start_tile = [&](uint32_t t, uint32_t at) {  // tile t's words (ring base at)
             const uint64_t tb = (uint64_t)t * kTile;
-            if (t < ti0 || t >= ti1) init_words<kTileWords, true>(S.ring, at, tb, pbase, P);
-            else init_words<kTileWords, false>(S.ring, at, tb, pbase, P);
+            if (t < ti0 || t >= ti1) {
+                init_words<kTileWords, true>(S.ring, at, tb, pbase, P);
+            } else if (kTmaStart) {
+                // one bulk copy (TMA) of the pattern words, from the shifted
+                // table copy that makes the source 16-byte aligned
+                if (threadIdx.x == 0) {
+                    const uint32_t r = pbase & 3u;
+                    const uint32_t bar = smem_addr(&S.mbar_start);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                                 "r"((uint32_t)kTileWords * 4)
+                                 : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            ring_addr + 4 * at),
+                        "l"(P.pattern + r * kPatStride + (pbase - r)), "r"((uint32_t)kTileWords * 4),
+                        "r"(bar)
+                        : "memory");
+                    start_pending = true;
+                }
+            } else {
+                init_words<kTileWords, false>(S.ring, at, tb, pbase, P);
+            }
             pbase += kTileWords;
             if (pbase >= kPatWords) pbase -= kPatWords;
+        };
+        // thread 0, before the barrier that publishes a start: its copy has landed
+        auto finish_start = [&]() {
+            if (kTmaStart && threadIdx.x == 0 && start_pending) {
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile(
+                        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+                        "selp.u32 %0, 1, 0, p; }"
+                        : "=r"(done)
+                        : "r"(smem_addr(&S.mbar_start)), "r"(start_parity)
+                        : "memory");
+                start_parity ^= 1u;
+                start_pending = false;
+            }
         };
 
         // the halo just below tile t0: the tail of buffer t0 - 1
@@ -708,9 +767,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
 #if !SQF2K_SPLIT_PHASE
         // prologue: start t0; sieve t0 and start t0 + 1
         start_tile(t0, ring_base(t0));
+        finish_start();
         __syncthreads();
         sieve_tile(t0, ring_base(t0));
         if (t0 + 1 < t1) start_tile(t0 + 1, ring_base(t0 + 1));
+        finish_start();
         __syncthreads();
 
         // One phase per tile t, one barrier: scan t (reads t and the tail of
@@ -730,6 +791,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             if (!FUSED && threadIdx.x == 0)
                 asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
 #endif
+            finish_start();
             __syncthreads();
             hb = hb1;
             hb1 = hb2;
@@ -953,9 +1015,9 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
     // p = 3, 5, 7 pattern of this domain
     DevBuf &pattern = a.buf ? c.pattern_b : c.pattern;
     DevBuf &counts = a.buf ? c.tile_counts_b : c.tile_counts;
-    pattern.reserve((kPatWords + kTileWords) * 4);
+    pattern.reserve((size_t)kPatCopies * kPatStride * 4);
     launch_on(st, "pattern", pattern_kernel,
-              dim3((unsigned)std::min<uint64_t>(ceil_div(kPatWords + kTileWords, 256), c.sm_count * 8)), dim3(256),
+              dim3((unsigned)std::min<uint64_t>(ceil_div(kPatCopies * kPatStride, 256), c.sm_count * 8)), dim3(256),
               0, a.base_n, a.pattern_present, pattern.as<uint32_t>());
     const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);
     counts.reserve((n_bt + 1) * 4);
