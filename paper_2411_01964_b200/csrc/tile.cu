@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(256) bucket_kernel(
 // at ~9 lanes/cycle/SM on B200, the same rate as byte stores, so no byte
 // array and no pack pass).
 #ifndef SQF2K_SPLIT_PHASE
-#define SQF2K_SPLIT_PHASE 0
+#define SQF2K_SPLIT_PHASE 1
 #endif
 // live tiles per phase: t-2 .. t+2 (5), or t-3 .. t+2 with the split phase
 // (tiles started 3 ahead, warps up to one phase apart) -- see tile_kernel
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
     uint32_t scanned = 0;  // <= 128 per tile, < 2^21 tiles
     bool waited = false;
-    constexpr bool kTmaStart = SQF2K_TMA_START && !SQF2K_SPLIT_PHASE;
+    constexpr bool kTmaStart = SQF2K_TMA_START;
     bool start_pending = false;  // thread 0: a start's bulk copy is in flight
     uint32_t start_parity = 0;
     if (kTmaStart) {
@@ -805,8 +805,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
 #else
         // prologue: start t0 .. t0 + 2; sieve t0
         start_tile(t0, ring_base(t0));
+        finish_start();
         if (t0 + 1 < t1) start_tile(t0 + 1, ring_base(t0 + 1));
+        finish_start();
         if (t0 + 2 < t1) start_tile(t0 + 2, ring_base(t0 + 2));
+        finish_start();
         __syncthreads();
         sieve_tile(t0, ring_base(t0));
         __syncthreads();
@@ -822,6 +825,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             if (t > t0) mbar_wait(&S.mbar, (mbar_phase - 1) & 1u);
             if (t + 3 < t1) start_tile(t + 3, hb3);
             scan_phase(t, hb);
+            finish_start();  // the start is published by this phase's arrivals
             mbar_arrive(&S.mbar);
             ++mbar_phase;
             hb = hb1;
