@@ -16,6 +16,9 @@ namespace sqf2k {
 
 namespace {
 
+#ifndef SQF2K_WAIT_HINT_NS
+#define SQF2K_WAIT_HINT_NS 1000000
+#endif
 #ifndef SQF2K_TMA_START
 #define SQF2K_TMA_START 1
 #endif
@@ -203,14 +206,17 @@ __device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t coun
 __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
+// the waiting thread sleeps in hardware until the phase completes (or the
+// hint elapses) instead of re-issuing the poll
+constexpr uint32_t kWaitHintNs = SQF2K_WAIT_HINT_NS;
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
     uint32_t done = 0;
     while (!done)
         asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; "
             "selp.u32 %0, 1, 0, p; }"
             : "=r"(done)
-            : "r"(smem_addr(bar)), "r"(parity)
+            : "r"(smem_addr(bar)), "r"(parity), "r"(kWaitHintNs)
             : "memory");
 }
 #endif
