@@ -145,14 +145,13 @@ __global__ void __launch_bounds__(256) bucket_kernel(
 
 // -------------------------------------------------------------------------
 // Shared memory of a tile CTA.  The tile is sieved directly in packed form:
-// 32-bit words, one bit per odd slot, in a 4-tile ring -- tile t occupies
-// quarter (t & 3) and its halo (the previous tile's last 2^(k_eff-1) slots)
-// is the tail of quarter (t - 1) & 3; starting tile t + 1 (quarter
-// (t + 1) & 3) never touches what tile t's scan or deferred words read.  A
-// word starts as the p = 3, 5, 7 pattern; the medium and bucket primes clear
-// their hits with shared-memory atomics (random scatter: bank-conflict bound
-// at ~9 lanes/cycle/SM on B200, the same rate as byte stores, so no byte
-// array and no pack pass).
+// 32-bit words, one bit per odd slot, in a ring of kRingTiles tile buffers --
+// tile t occupies buffer t mod kRingTiles and its halo (the previous tile's
+// last 2^(k_eff-1) slots) is the tail of buffer t - 1.  A word starts as the
+// p = 3, 5, 7 pattern; the medium and bucket primes clear their hits with
+// shared-memory atomics (random scatter: bank-conflict bound at ~9
+// lanes/cycle/SM on B200, the same rate as byte stores, so no byte array and
+// no pack pass).
 #ifndef SQF2K_SPLIT_PHASE
 #define SQF2K_SPLIT_PHASE 1
 #endif
@@ -343,7 +342,7 @@ __device__ __forceinline__ void init_words(uint32_t *ring, uint32_t at, uint64_t
 // The pre-tile starts the H = HW*32 halo slots (HW in {32, 64, ..., 1024}).
 __device__ __forceinline__ void init_halo(uint32_t *ring, uint32_t at, uint32_t HW, uint64_t base,
                                           uint32_t pbase, const TileParams &P) {
-    static_assert(kHaloWordsMax <= 1024 && kHaloWordsMax <= kTileWords, "halo within a quarter");
+    static_assert(kHaloWordsMax <= 1024 && kHaloWordsMax <= kTileWords, "halo within a buffer");
     if (HW == 1024) init_words<1024, true>(ring, at, base, pbase, P);
     else if (HW == 512) init_words<512, true>(ring, at, base, pbase, P);
     else if (HW == 256) init_words<256, true>(ring, at, base, pbase, P);
@@ -416,7 +415,7 @@ __device__ __forceinline__ uint32_t scan_word(uint32_t pend, uint32_t prv, uint3
     return pend;
 }
 
-// Exponent passes over the tile (ring quarter at hb): thread t owns the
+// Exponent passes over the tile (ring buffer at hb): thread t owns the
 // kWordsPerThread consecutive words from W*t, taken 4 at a time (one LDS.128
 // plus the left neighbour).  EDGE masks the scan range, TRACK records per-k
 // least slots while this CTA still lacks them.  Words left after KMAIN passes
@@ -533,11 +532,11 @@ __device__ __forceinline__ void finish_call(TileSmem &S, const TileParams &P) {
 }
 
 // KMAIN = min(k_eff, 5) unconditional passes; the export form ignores it.
-// Per tile t, two phases between barriers:
-//   X(t): clear the medium and bucket primes' hits in quarter t & 3;
-//   Y(t): scan tile t (fused) or store it (export), finish tile t - 1's
-//         deferred words, and start tile t + 1's words from the pattern in
-//         quarter (t + 1) & 3 -- nothing in Y(t) reads that quarter.
+// Per tile t (split phase, the default): sieve t + 1, wait for every warp to
+// finish phase t - 1 (mbarrier), start t + 3 (TMA bulk copy of the pattern),
+// scan t (fused) or store it (export, TMA bulk store), finish t - 1's
+// deferred words, arrive.  Without the split phase: one barrier per tile,
+// scan t + sieve t + 1 + start t + 2 between barriers.
 // Per-CTA timeline for experiment builds (-DSQF2K_EXP_TIMELINE, tools/timeline.py).
 #ifdef SQF2K_EXP_TIMELINE
 __device__ unsigned long long g_timeline[4096][4];

@@ -7,7 +7,7 @@
 // Per tile a CTA sieves the tile directly in packed form (one bit per odd
 // slot, 32-bit LSB-first words in shared memory):
 //   1. each word starts as the periodic mask of p = 3, 5, 7 (one table word
-//      per u-word mod 9*25*49);
+//      per u-word mod 9*25*49; a whole tile by one TMA bulk copy);
 //   2. the odd multiples of p^2 are cleared with shared-memory atomic ANDs --
 //      medium primes 11 <= p < kPMed from per-lane "descriptors" whose next
 //      hit offset lives in a register across tiles (no division, no table
@@ -16,7 +16,8 @@
 //      over the words -- passes 1..5 unconditionally for every word (funnel
 //      shifts of the word and its left neighbour), the rare remainder
 //      divergently -- reading n - 2^k from the tile or the previous tile's
-//      tail (2^(k_eff-1) slots of halo); export mode: stores the words.
+//      tail (2^(k_eff-1) slots of halo); export mode: stores the words (one
+//      TMA bulk copy per tile).
 #pragma once
 
 #include <stdint.h>
