@@ -221,6 +221,13 @@ void enqueue_verify(const VerifyPlan &pl) {
     fork_side();
     SQF2K_CUDA(cudaMemsetAsync(acc, 0, sizeof(Acc), c.side));
     SQF2K_CUDA(cudaMemsetAsync(acc->min_n, 0xff, sizeof acc->min_n, c.side));
+    // the tile scheduler's words reset themselves (last CTA); also cleared per
+    // call so an aborted launch cannot leak a stale state (off the critical path)
+    if (!c.sched.ptr) {
+        c.sched.reserve(64);
+        SQF2K_CUDA(cudaMemset(c.sched.ptr, 0, 64));
+    }
+    SQF2K_CUDA(cudaMemsetAsync(c.sched.ptr, 0, 64, c.side));
     prep_tile_batch(a, c.side);
     generate_primes_async(pl.limit);
     a.primes = c.primes_u32.as<uint32_t>();  // (re)allocated by the generator
