@@ -642,7 +642,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         MedLane L;
         init_medium(L, P, b0);
         if (threadIdx.x < 2) S.n_res[threadIdx.x] = 0;
-        uint32_t pbase = (uint32_t)((b0 / 32) % kPatWords);  // pattern index of the next start
+        // pattern index of the next tile start (t0 first; the halo has its own)
+        uint32_t pbase = (uint32_t)(((uint64_t)t0 * kTileWords) % kPatWords);
+        const uint32_t pbase_halo = (uint32_t)((b0 / 32) % kPatWords);
         auto start_tile = [&](uint32_t t, uint32_t at) {  // tile t's words (ring base at)
             const uint64_t tb = (uint64_t)t * kTile;
             if (t < ti0 || t >= ti1) {
@@ -686,19 +688,57 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                 start_pending = false;
             }
         };
+        // tiles ta .. ta+n-1 started together: one expect_tx for their bulk
+        // copies (one wait), edge tiles by the masked per-thread path
+        auto start_batch = [&](uint32_t ta, uint32_t n) {
+            auto edge_t = [&](uint32_t t) { return t < ti0 || t >= ti1; };
+            uint32_t bytes = 0;
+            for (uint32_t i = 0; i < n; ++i)
+                if (!edge_t(ta + i)) bytes += (uint32_t)kTileWords * 4;
+            if (kTmaStart && bytes && threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                                 smem_addr(&S.mbar_start)),
+                             "r"(bytes)
+                             : "memory");
+                start_pending = true;
+            }
+            for (uint32_t i = 0; i < n; ++i) {
+                const uint32_t t = ta + i, at = ring_base(t);
+                const uint64_t tb = (uint64_t)t * kTile;
+                if (edge_t(t)) {
+                    init_words<kTileWords, true>(S.ring, at, tb, pbase, P);
+                } else if (kTmaStart) {
+                    if (threadIdx.x == 0) {
+                        const uint32_t r = pbase & 3u;
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                ring_addr + 4 * at),
+                            "l"(P.pattern + r * kPatStride + (pbase - r)),
+                            "r"((uint32_t)kTileWords * 4), "r"(smem_addr(&S.mbar_start))
+                            : "memory");
+                    }
+                } else {
+                    init_words<kTileWords, false>(S.ring, at, tb, pbase, P);
+                }
+                pbase += kTileWords;
+                if (pbase >= kPatWords) pbase -= kPatWords;
+            }
+        };
+#if SQF2K_SPLIT_PHASE
+        start_batch(t0, min(3u, t1 - t0));  // in flight during the halo work below
+#endif
 
         // the halo just below tile t0: the tail of buffer t0 - 1
         const uint32_t halo_at = ring_base(t0 + kRingTiles - 1) + kTileWords - HW;
         if (FUSED) {
             if (pre) {  // pre-tile: sieve the H slots below the chunk
-                init_halo(S.ring, halo_at, HW, b0, pbase, P);
+                init_halo(S.ring, halo_at, HW, b0, pbase_halo, P);
                 __syncthreads();
                 scatter_medium(L, ring_addr + 4 * halo_at, H);
                 if (!waited) grid_dependency_wait();  // bucket lists from here on
                 waited = true;
                 scatter_bucket(ring_addr + 4 * halo_at, P, t0 - 1, kTile - H);
-                pbase += HW;
-                if (pbase >= kPatWords) pbase -= kPatWords;
             } else {
                 for (uint32_t i = threadIdx.x; i < HW; i += kThreads) S.ring[halo_at + i] = 0u;
             }
@@ -808,12 +848,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         if (!FUSED && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #endif
 #else
-        // prologue: start t0 .. t0 + 2; sieve t0
-        start_tile(t0, ring_base(t0));
-        finish_start();
-        if (t0 + 1 < t1) start_tile(t0 + 1, ring_base(t0 + 1));
-        finish_start();
-        if (t0 + 2 < t1) start_tile(t0 + 2, ring_base(t0 + 2));
+        // prologue: starts t0 .. t0 + 2 (issued before the halo); sieve t0
         finish_start();
         __syncthreads();
         sieve_tile(t0, ring_base(t0));
