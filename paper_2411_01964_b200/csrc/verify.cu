@@ -99,7 +99,7 @@ struct SmallSet {
     uint32_t present = 0;
 };
 
-SmallSet small_set_upto(uint64_t limit) {
+SmallSet small_set_upto_impl(uint64_t limit) {
     static const std::vector<uint32_t> all = small_primes(kPMed);
     SmallSet s;
     for (uint32_t p : all) {
@@ -111,6 +111,14 @@ SmallSet small_set_upto(uint64_t limit) {
         else if (p >= 11) s.med.push_back(p);
     }
     return s;
+}
+
+SmallSet small_set_upto(uint64_t limit) {
+    if (limit >= kPMed) {  // every range above 2^20: the full set, built once
+        static const SmallSet full = small_set_upto_impl(kPMed);
+        return full;
+    }
+    return small_set_upto_impl(limit);
 }
 
 }  // namespace
