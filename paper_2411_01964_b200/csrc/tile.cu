@@ -16,6 +16,9 @@ namespace sqf2k {
 
 namespace {
 
+#ifndef SQF2K_WAIT_SLEEP_NS
+#define SQF2K_WAIT_SLEEP_NS 0
+#endif
 #ifndef SQF2K_WAIT_HINT_NS
 #define SQF2K_WAIT_HINT_NS 1000000
 #endif
@@ -208,15 +211,19 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
 // the waiting thread sleeps in hardware until the phase completes (or the
 // hint elapses) instead of re-issuing the poll
 constexpr uint32_t kWaitHintNs = SQF2K_WAIT_HINT_NS;
+constexpr uint32_t kWaitSleepNs = SQF2K_WAIT_SLEEP_NS;
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
     uint32_t done = 0;
-    while (!done)
+    for (;;) {
         asm volatile(
             "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; "
             "selp.u32 %0, 1, 0, p; }"
             : "=r"(done)
             : "r"(smem_addr(bar)), "r"(parity), "r"(kWaitHintNs)
             : "memory");
+        if (done) break;
+        if (kWaitSleepNs) __nanosleep(kWaitSleepNs);  // leave the issue slots to working warps
+    }
 }
 #endif
 
