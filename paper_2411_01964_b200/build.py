@@ -41,7 +41,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return LIB
     tmp = LIB.with_name(f".{LIB.name}.{os.getpid()}.tmp")
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", str(INCLUDE), "-o", str(tmp),
+    extra = os.environ.get("SQF2K_NVCC_EXTRA", "").split()  # build options, e.g. -DSQF2K_...=1
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", str(INCLUDE), "-o", str(tmp),
            *[str(CSRC / s) for s in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

@@ -172,7 +172,7 @@ struct TileSmem {
     unsigned long long first[kDepthMax + 1];
     uint32_t first_t[2][6];       // k <= 5: least tile-local slot of tile t (buffer t & 1)
     uint32_t need;                // bit k: least n with exponent k still unknown
-    uint32_t cnt[kDepthMax + 1];  // counts of k > kMainMax (rare)
+    uint32_t cnt[kDepthMax + 1];  // counts of k > kMainMax (rare); [0]: slots left after the main passes
     // words left after the main passes of tile t (queue t & 1), finished
     // while tile t + 1 is scanned
     uint32_t res_w[2][kResCap], res_p[2][kResCap];
@@ -393,32 +393,39 @@ __device__ __forceinline__ void scan_residue(TileSmem &S, const TileParams &P, u
     }
 }
 
-// One pass of the main scan on one word; k = 1 is not counted (hist[1] is
-// derived from the scanned-slot count by conservation, see verify.cu).
-// One pass of the main scan on one word; k = 1 is not counted (hist[1] is
-// derived from the scanned-slot count by conservation, see verify.cu).
-// TRACK: the thread's least slot with exponent k (its words come in slot
-// order, so the first hit is the least); reduced per warp after the tile.
-template <bool TRACK, bool COUNT>
-__device__ __forceinline__ void pass(uint32_t &pend, uint32_t sl, uint32_t &cnt, uint32_t &fk,
-                                     uint32_t wl) {
-    const uint32_t nw = pend & sl;
-    if (COUNT) cnt += __popc(nw);
-    if (TRACK && nw && fk == ~0u) fk = 32 * wl + __ffs(nw) - 1;
-    pend &= ~sl;
-}
-
 // Main scan of one word (cur, its left neighbour prv): n - 2^k for k <= 5 is
 // 2^(k-1) slots back, inside (cur, prv).  Returns the slots left after KMAIN
-// passes.
+// passes.  Counting: c[k] (k < KMAIN) accumulates the slots still pending
+// after pass k -- the histogram is the difference of consecutive entries,
+// the (rare) leftover path subtracts its slots from hist[KMAIN] (S.cnt[0]) and hist[1] is derived from
+// the scanned-slot count by conservation (verify.cu).  The covered bits are
+// counted (pending = 32 - covered; no NOT in front of the POPC; masked edge
+// slots count as covered) and the 32 per word are added back per tile.
+// TRACK: the thread's least slot with exponent k (its words come in slot
+// order, so the first hit is the least); reduced per warp after the tile.
 template <bool TRACK, int KMAIN>
 __device__ __forceinline__ uint32_t scan_word(uint32_t pend, uint32_t prv, uint32_t cur,
                                               uint32_t (&c)[6], uint32_t (&f)[6], uint32_t wl) {
-    pass<TRACK, false>(pend, __funnelshift_l(prv, cur, 1), c[1], f[1], wl);
-    if (KMAIN >= 2) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 2), c[2], f[2], wl);
-    if (KMAIN >= 3) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 4), c[3], f[3], wl);
-    if (KMAIN >= 4) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 8), c[4], f[4], wl);
-    if (KMAIN >= 5) pass<TRACK, true>(pend, __funnelshift_l(prv, cur, 16), c[5], f[5], wl);
+#pragma unroll
+    for (int k = 1; k <= KMAIN; ++k) {
+        const uint32_t sl = __funnelshift_l(prv, cur, 1u << (k - 1));
+        if (TRACK) {
+            const uint32_t nw = pend & sl;
+            if (nw && f[k] == ~0u) f[k] = 32 * wl + __ffs(nw) - 1;
+        }
+        pend &= ~sl;
+        if (k < KMAIN) c[k] -= __popc(~pend);  // + 32 per word: scan_tile
+    }
+    return pend;
+}
+
+// Scan-range mask of the word starting at tile slot u0 (EDGE tiles only).
+__device__ __forceinline__ uint32_t edge_mask(const TileParams &P, uint64_t u0) {
+    if (u0 + 32 <= P.scan_lo || u0 >= P.U) return 0u;
+    uint32_t pend = ~0u;
+    if (u0 < P.scan_lo) pend &= ~0u << (uint32_t)(P.scan_lo - u0);
+    if (u0 + 32 > P.U) pend &= (1u << (uint32_t)(P.U - u0)) - 1u;
+    if (P.one_u >= u0 && P.one_u < u0 + 32) pend &= ~(1u << (uint32_t)(P.one_u - u0));
     return pend;
 }
 
@@ -456,23 +463,22 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
         uint32_t left[CW], any = 0;
 #pragma unroll
         for (int i = 0; i < CW; ++i) {
-            const uint64_t u0 = tb + 32ull * (w0 + i);
             uint32_t pend = ~0u;
             if (EDGE) {
-                if (u0 + 32 <= P.scan_lo || u0 >= P.U) {
-                    pend = 0u;
-                } else {
-                    if (u0 < P.scan_lo) pend &= ~0u << (uint32_t)(P.scan_lo - u0);
-                    if (u0 + 32 > P.U) pend &= (1u << (uint32_t)(P.U - u0)) - 1u;
-                    if (P.one_u >= u0 && P.one_u < u0 + 32) pend &= ~(1u << (uint32_t)(P.one_u - u0));
-                }
+                pend = edge_mask(P, tb + 32ull * (w0 + i));
                 scanned += __popc(pend);
             }
             left[i] = scan_word<TRACK, KMAIN>(pend, prv[i], cur[i], c, f, w0 + i);
             any |= left[i];
         }
         if (!EDGE) scanned += 32 * CW;
-        if (any) {
+        if (any) {  // rare
+            if (KMAIN >= 2) {  // pending after pass KMAIN: subtracted from hist[KMAIN] at the end
+                uint32_t nl = 0;
+#pragma unroll
+                for (int i = 0; i < CW; ++i) nl += __popc(left[i]);
+                atomicAdd(&S.cnt[0], nl);
+            }
 #pragma unroll
             for (int i = 0; i < CW; ++i) {
                 if (!left[i]) continue;
@@ -493,6 +499,8 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
             }
         }
     }
+#pragma unroll
+    for (int k = 1; k < KMAIN; ++k) c[k] += 32 * W;  // pending = 32 - covered per word
     if (TRACK) {  // per k: one warp reduction, one shared atomic
 #pragma unroll
         for (int k = 1; k <= KMAIN; ++k) {
@@ -907,10 +915,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         }
         const int lane = threadIdx.x & 31;
 #pragma unroll
-        for (int k = 2; k <= 5; ++k) {
-            const uint32_t s = __reduce_add_sync(0xffffffffu, c[k]);
+        for (int k = 2; k <= KMAIN; ++k) {  // met at k: pending after k - 1, not after k
+            const uint32_t s = __reduce_add_sync(0xffffffffu, c[k - 1] - c[k]);
             if (lane == 0 && s) atomicAdd(&P.hist[k], (unsigned long long)s);
         }
+        if (KMAIN >= 2 && threadIdx.x == 0 && S.cnt[0])  // (mod 2^64: the sum comes out right)
+            atomicAdd(&P.hist[KMAIN], 0ull - (unsigned long long)S.cnt[0]);
         const unsigned long long sc = __reduce_add_sync(0xffffffffu, scanned);
         if (lane == 0 && sc) atomicAdd(P.scanned, sc);
         if (threadIdx.x > kMainMax && threadIdx.x <= kDepthMax && S.cnt[threadIdx.x])
