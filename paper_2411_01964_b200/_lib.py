@@ -145,6 +145,12 @@ def lib() -> ctypes.CDLL:
     return L
 
 
+def bound_device() -> int:
+    """The CUDA device this process's library is bound to (binds it if needed)."""
+    lib()
+    return int(_device)
+
+
 def ptr(a: np.ndarray | None):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 

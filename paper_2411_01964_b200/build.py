@@ -23,7 +23,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["context.cu", "primes.cu", "tile.cu", "verify.cu", "scan.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
-         "--expt-relaxed-constexpr", "-shared", "-cudart", "static", "-diag-suppress", "186"]
+         "--expt-relaxed-constexpr", "-diag-suppress", "186"]
+OBJ = PKG / "_obj"
 
 
 def _inputs() -> list[Path]:
@@ -38,16 +39,35 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Each source compiles to an object in parallel (no cross-file device
+    code: relocatable device code is not needed), then one host link."""
     if not force and up_to_date():
         return LIB
-    tmp = LIB.with_name(f".{LIB.name}.{os.getpid()}.tmp")
+    from concurrent.futures import ThreadPoolExecutor
+
+    OBJ.mkdir(exist_ok=True)
     extra = os.environ.get("SQF2K_NVCC_EXTRA", "").split()  # build options, e.g. -DSQF2K_...=1
-    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", str(INCLUDE), "-o", str(tmp),
-           *[str(CSRC / s) for s in SOURCES]]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+    tag = f"{os.getpid()}"
+
+    def compile_one(src: str) -> Path:
+        obj = OBJ / f"{Path(src).stem}.{tag}.o"
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", str(INCLUDE), "-c", "-o", str(obj),
+               str(CSRC / src)]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
+    tmp = LIB.with_name(f".{LIB.name}.{tag}.tmp")
+    try:
+        subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp),
+                        *map(str, objs)], check=True)
+    finally:
+        for o in objs:
+            o.unlink(missing_ok=True)
     os.replace(tmp, LIB)
     return LIB
 

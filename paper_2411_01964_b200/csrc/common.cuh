@@ -235,6 +235,7 @@ constexpr uint64_t kMaxEnd = 1ULL << 62;
 // PrimeInfo split into ctx().prime_info, without a host sync (async) or
 // returning the count (sync).
 void generate_primes_async(uint64_t limit);
+void ensure_primes(uint64_t limit);
 uint64_t generate_primes_device(uint64_t limit);
 // Upper bound of pi(x) (Rosser-Schoenfeld), for buffer sizing without a sync.
 uint64_t pi_upper(uint64_t x);

@@ -347,6 +347,16 @@ void generate_primes_async(uint64_t limit) {
            offsets + nseg, info);
 }
 
+// The table only if the cached one does not already hold every prime <=
+// limit (a larger table is fine for trial division: warp_squarefree stops at
+// p^2 > m).  The verify path always regenerates (a run builds its table,
+// runner.py:192); recheck and is_squarefree reuse it.
+void ensure_primes(uint64_t limit) {
+    Context &c = ctx();
+    if (c.primes_limit >= std::max<uint64_t>(limit, 2)) return;
+    generate_primes_async(limit);
+}
+
 // Generate every prime <= limit into ctx.primes_u32; returns the count.
 uint64_t generate_primes_device(uint64_t limit) {
     Context &c = ctx();

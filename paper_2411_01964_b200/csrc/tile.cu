@@ -196,6 +196,13 @@ __device__ __forceinline__ void clear_bit(uint32_t wbase, uint32_t o) {
 #endif
 }
 
+__device__ __forceinline__ unsigned long long warp_sum_u64(uint32_t x) {
+    unsigned long long v = x;
+#pragma unroll
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -617,8 +624,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     if (threadIdx.x < 12) S.first_t[threadIdx.x / 6][threadIdx.x % 6] = ~0u;
     if (threadIdx.x == 0) S.need = ~0u;
     const uint32_t ring_addr = smem_addr(S.ring);
+    // per-thread counters: each adds <= 32 * kWordsPerThread = 256 per tile, and
+    // run_tile_batch keeps a CTA under 2^23 tiles, so they stay below 2^31; the
+    // warp sums at the end are 64-bit
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
-    uint32_t scanned = 0;  // <= 128 per tile, < 2^21 tiles
+    uint32_t scanned = 0;
     bool waited = false;
     constexpr bool kTmaStart = SQF2K_TMA_START;
     bool start_pending = false;  // thread 0: a start's bulk copy is in flight
@@ -916,12 +926,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         const int lane = threadIdx.x & 31;
 #pragma unroll
         for (int k = 2; k <= KMAIN; ++k) {  // met at k: pending after k - 1, not after k
-            const uint32_t s = __reduce_add_sync(0xffffffffu, c[k - 1] - c[k]);
-            if (lane == 0 && s) atomicAdd(&P.hist[k], (unsigned long long)s);
+            const unsigned long long s = warp_sum_u64(c[k - 1] - c[k]);
+            if (lane == 0 && s) atomicAdd(&P.hist[k], s);
         }
         if (KMAIN >= 2 && threadIdx.x == 0 && S.cnt[0])  // (mod 2^64: the sum comes out right)
             atomicAdd(&P.hist[KMAIN], 0ull - (unsigned long long)S.cnt[0]);
-        const unsigned long long sc = __reduce_add_sync(0xffffffffu, scanned);
+        const unsigned long long sc = warp_sum_u64(scanned);
         if (lane == 0 && sc) atomicAdd(P.scanned, sc);
         if (threadIdx.x > kMainMax && threadIdx.x <= kDepthMax && S.cnt[threadIdx.x])
             atomicAdd(&P.hist[threadIdx.x], (unsigned long long)S.cnt[threadIdx.x]);
@@ -1117,6 +1127,7 @@ void bucket_batch(const BatchArgs &a, cudaStream_t st) {
 // prime table), on the library stream.
 void run_tile_batch(const BatchArgs &a) {
     Context &c = ctx();
+    if (a.U > (1ull << 41)) throw Error{SQF2K_EINVAL, "batch domain above 2^41 slots"};
     const uint32_t n_tiles = (uint32_t)ceil_div(a.U, kTile);
     const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);
 
@@ -1192,6 +1203,8 @@ void run_tile_batch(const BatchArgs &a) {
     const size_t smem = tile_smem_bytes();
     uint64_t grid_cap = (uint64_t)c.sm_count * kCtasPerSm;
     if (const char *g = std::getenv("SQF2K_DEBUG_GRID")) grid_cap = std::max(1, atoi(g));
+    // at least ceil(n_tiles / 2^23) CTAs: the per-thread 32-bit counters
+    grid_cap = std::max<uint64_t>(grid_cap, ceil_div(n_tiles, 1ull << 23));
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(n_tiles, grid_cap));
     if (a.fused) {
         const uint32_t kmain = std::min<uint32_t>(a.k_eff, kMainMax);

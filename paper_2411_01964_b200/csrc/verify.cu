@@ -32,6 +32,7 @@ void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_sl
 namespace {
 
 constexpr uint64_t kDefaultBatch = 1ull << 36;
+constexpr uint64_t kMaxBatch = 1ull << 40;
 
 // Escalation: n unresolved at the tile depth, exponents k_from..k_max exactly.
 __global__ void escalate_kernel(const unsigned long long *__restrict__ esc,
@@ -319,7 +320,10 @@ void plan_key(const VerifyPlan &pl, uint64_t key[8]) {
     key[4] = pl.esc_cap;
     key[5] = pl.dev_fail_cap;
     key[6] = pl.H;
-    key[7] = 0;
+    // the tile grid is read from SQF2K_DEBUG_GRID at enqueue time: a replayed
+    // graph must have been captured under the same cap
+    const char *g = std::getenv("SQF2K_DEBUG_GRID");
+    key[7] = g ? (uint64_t)std::max(1, atoi(g)) : 0;
 }
 
 GraphEntry *find_graph(const uint64_t key[8]) {
@@ -381,6 +385,9 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
     pl.k_max = k_max;
     pl.k_eff = std::min(k_max, depth);
     pl.H = std::max<uint32_t>(1024u, 1u << (pl.k_eff - 1));
+    if (o.batch_slots > kMaxBatch)
+        return fail(SQF2K_EINVAL, "batch_slots must be at most 2^40, got %llu",
+                    (unsigned long long)o.batch_slots);
     pl.batch = std::max<uint64_t>(o.batch_slots ? o.batch_slots : kDefaultBatch, (uint64_t)kTile);
     pl.n_slots = (end - start) / 2;
     pl.limit = isqrt_u64(end - 1);
@@ -398,6 +405,7 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
         GraphEntry *g = graphs ? find_graph(key) : nullptr;
         if (g) {
             SQF2K_CUDA(cudaGraphLaunch(g->exec, c.stream));
+            c.primes_limit = pl.limit;  // the replay rebuilt this call's table
             c.h2d_bytes += g->h2d;
             c.d2h_bytes += g->d2h;
         } else {
@@ -526,7 +534,7 @@ int sieve_bits(uint64_t start, uint64_t end, const int64_t *primes_h, uint64_t n
 int recheck(const uint64_t *n, uint64_t count, uint64_t prime_limit, int32_t *k_out) {
     Context &c = ctx();
     if (!count) return SQF2K_OK;
-    generate_primes_async(prime_limit);
+    ensure_primes(prime_limit);
     c.esc.reserve(count * 8);
     c.fail.reserve(count * 4);
     copy_h2d(c.esc.ptr, n, count * 8);
@@ -541,7 +549,7 @@ int recheck(const uint64_t *n, uint64_t count, uint64_t prime_limit, int32_t *k_
 int is_squarefree(const uint64_t *n, uint64_t count, uint64_t prime_limit, uint8_t *out) {
     Context &c = ctx();
     if (!count) return SQF2K_OK;
-    generate_primes_async(prime_limit);
+    ensure_primes(prime_limit);
     c.esc.reserve(count * 8);
     c.fail.reserve(count + 16);
     copy_h2d(c.esc.ptr, n, count * 8);

@@ -391,3 +391,46 @@ def test_top_of_domain_window():
         assert got.k_sum == want["k_sum"]
         assert got.record_candidates == want["record_candidates"]
         assert got.failures == want["failures"]
+
+
+# -- C4 / C5: reports pinned to process-sharded reference runs -------------------
+
+def _window_golden(log2w):
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", f"golden_window_2p{log2w}.json")
+    if not os.path.exists(p):
+        pytest.skip(f"golden_window_2p{log2w}.json not generated yet")
+    return json.load(open(p))
+
+
+@pytest.mark.parametrize("log2w", [40, 44])
+def test_window_report_matches_reference(log2w):
+    # C4 = [2^50 - 2^40 + 1, 2^50), C5 = [2^50 - 2^44 + 1, 2^50): the whole
+    # report JSON (histogram, k_sum, odd_scanned, k_max_observed) against the
+    # merged reference shards (tests/golden/make_golden_window.py)
+    g = _window_golden(log2w)
+    cfg = g["config"]
+    for pipeline in (("fused", "bitmap") if log2w == 40 else ("fused",)):
+        rep = run_verify(RunConfig(start=cfg["start"], end=cfg["end"], pipeline=pipeline))
+        assert render_report_json(rep) == g["report_json"], pipeline
+        want = g["summary"]
+        assert {str(m): n for m, n in rep.summary.record_candidates.items()} == want["record_candidates"]
+
+
+@pytest.mark.parametrize("log2w", [40, 44])
+def test_window_shards_match_reference(log2w):
+    # individual 2^34-integer reference runs (summaries incl. record candidates)
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", f"golden_window_2p{log2w}.partial.jsonl")
+    if not os.path.exists(p):
+        pytest.skip("no shard file")
+    rows = [json.loads(x) for x in open(p).read().splitlines() if x.strip()]
+    rng = random.Random(log2w)
+    for r in rng.sample(rows, min(6, len(rows))):
+        got = run_verify(RunConfig(start=r["start"], end=r["end"])).summary
+        want = r["summary"]
+        assert got.start == want["start"] and got.end == want["end"]
+        assert {str(k): c for k, c in enumerate(got.histogram) if c} == want["histogram"]
+        assert got.k_sum == want["k_sum"]
+        assert {str(m): n for m, n in got.record_candidates.items()} == want["record_candidates"]
+        assert got.failures == want["failures"]

@@ -81,3 +81,26 @@ def test_shard_bounds_partition():
     with pytest.raises(ValueError):
         shard_bounds(1, 11, 2, 2)
     assert len(SegmentSummary.empty().histogram) == HIST_MAX_K + 1
+
+
+def test_pack_unpack_roundtrip():
+    from paper_2411_01964_b200.shard import pack_summary, unpack_summary
+
+    h = [0] * (HIST_MAX_K + 1)
+    h[1], h[2], h[7] = 10, 4, 1
+    s = SegmentSummary(101, 151, h, 10 + 8 + 7, 7, {1: 103, 2: 131, 3: 131}, [141, 145])
+    sums, mins = pack_summary(s)
+    assert len(sums) == len(mins) - 1 == HIST_MAX_K + 2
+    back = unpack_summary(sums, mins, [145, 141])
+    assert back == s
+    e_sums, e_mins = pack_summary(SegmentSummary.empty())
+    assert unpack_summary(e_sums, e_mins, []) == SegmentSummary.empty()
+    # reduction of two packed buffers = merge of the summaries
+    from paper_2411_01964_b200.aggregate import merge
+    h2 = [0] * (HIST_MAX_K + 1)
+    h2[1], h2[3] = 5, 2
+    t = SegmentSummary(151, 171, h2, 11, 3, {1: 153, 2: 153}, [])
+    ts, tm = pack_summary(t)
+    red = unpack_summary([a + b for a, b in zip(sums, ts)], [min(a, b) for a, b in zip(mins, tm)],
+                         s.failures + t.failures)
+    assert red == merge(s, t)
