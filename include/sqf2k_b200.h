@@ -22,8 +22,8 @@
  *     (so p <= 2^31 and p^2 < 2^62); larger ends are SQF2K_EINVAL.
  *   - Bit layout of segment bitmaps is the reference's: slot i = (n-start)/2,
  *     bit i lives in byte i>>3 at position i&7 (LSB first), 1 = squarefree,
- *     buffers padded with zero bits to a multiple of 8 bytes (sieve.py:53-56,
- *     sieve.py:100-109).
+ *     buffers padded with zero bits to a multiple of 8 bytes (sieve.py:13-16,
+ *     sieve.py:60-69).
  */
 #ifndef SQF2K_B200_H
 #define SQF2K_B200_H
@@ -54,7 +54,7 @@ enum {
  * Mergeable scan summary -- the device-side form of SegmentSummary
  * (aggregate.py:25-62).  The GPU produces hist[] and min_n[]; the library
  * derives k_sum, k_max_observed and the record candidates from them exactly
- * as the reference's per-block loop does (search.py:368-381):
+ * as the reference's per-block loop does (search.py:187-200):
  *   cand[m] = least n in the range whose smallest exponent exceeds m
  *           = min( min_{m < k <= k_max} min_n[k], least failure ),
  *   defined for 1 <= m <= k_max whenever such an n exists.
@@ -116,17 +116,17 @@ int sqf2k_prime_count(uint64_t limit, uint64_t *count);
  * cap = capacity of out; *count = number written (== pi(limit)).          */
 int sqf2k_primes(uint64_t limit, int64_t *out, uint64_t cap, uint64_t *count);
 
-/* ---- L1: segment sieve  (replaces sieve.py:112-151 sieve_segment) ------ */
+/* ---- L1: segment sieve  (replaces sieve.py:72-111 sieve_segment) ------ */
 
 /* Squarefree flags of the odd n in [start, end) packed LSB-first into
  * nbytes = ceil(n_slots/64)*8 bytes, using the caller's prime table
- * (ascending int64, must cover isqrt(end-1): sieve.py:126-128).          */
+ * (ascending int64, must cover isqrt(end-1): sieve.py:86-88).          */
 int sqf2k_sieve_bits(uint64_t start, uint64_t end, const int64_t *primes,
                      uint64_t n_primes, uint8_t *out, uint64_t nbytes);
 
 /* ---- L2: min-k scan over a two-segment window
- *      (replaces search.py:400-433 scan_segment and search.py:436-460
- *       scan_exponents; window rules of search.py:278-316) --------------- */
+ *      (replaces search.py:219-252 scan_segment and search.py:255-279
+ *       scan_exponents; window rules of search.py:97-135) --------------- */
 
 /* prev_bits == NULL means "no predecessor" (start of a run at n = 1).
  * Bit buffers use the Segment layout above.  failures receives the n left
@@ -143,7 +143,7 @@ int sqf2k_scan_exponents(const uint8_t *prev_bits, uint64_t prev_start,
                          uint8_t *kvals, uint64_t n_slots);
 
 /* ---- L4 hot loop: verify a whole range on the GPU
- *      (replaces the segment loop of runner.py:583-633: prime table,
+ *      (replaces the segment loop of runner.py:216-252: prime table,
  *       predecessor seeding, sieve, scan and merge of every segment) ----- */
 
 /* Smallest exponent of every odd n in [start, end), n = 1 excluded, up to
@@ -163,7 +163,7 @@ int sqf2k_recheck(const uint64_t *n, uint64_t count, uint64_t prime_limit,
                   int32_t *k_out);
 
 /* Squarefree flag of each n[i] >= 1 by exact trial division on the GPU
- * (replaces sieve.py:154-171 is_squarefree_oracle); same prime rule.   */
+ * (replaces sieve.py:114-131 is_squarefree_oracle); same prime rule.   */
 int sqf2k_is_squarefree(const uint64_t *n, uint64_t count, uint64_t prime_limit,
                         uint8_t *out);
 

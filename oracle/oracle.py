@@ -8,7 +8,7 @@ falling back here.
 
 Return values mirror the reference's Python types so tests compare like
 for like: prime tables are int64 numpy arrays (primes.py:11-16), segment
-bits are padded uint8 arrays (sieve.py:59-65), summaries are dicts with the
+bits are padded uint8 arrays (sieve.py:19-25), summaries are dicts with the
 SegmentSummary fields (aggregate.py:25-41).
 """
 
@@ -98,7 +98,7 @@ def generate_primes(limit: int) -> np.ndarray:
 
 
 def sieve_bits(start: int, end: int, primes: np.ndarray, limit: int) -> np.ndarray:
-    """sieve.py:149-151 sieve_segment(...).bits"""
+    """sieve.py:109-111 sieve_segment(...).bits"""
     n_slots = (end - start) // 2 if end > start else 0
     nbytes = ((n_slots + 63) // 64) * 8
     out = np.zeros(max(nbytes, 8), dtype=np.uint8)
@@ -152,7 +152,7 @@ def _call_with_failures(fn, cap: int = 1 << 12):
 def scan_window(prev: tuple[int, int, np.ndarray] | None,
                 cur: tuple[int, int, np.ndarray], k_max: int,
                 block_slots: int = 1 << 20) -> dict:
-    """search.py:400-433 scan_segment over SegmentWindow(prev, cur)."""
+    """search.py:219-252 scan_segment over SegmentWindow(prev, cur)."""
     ps, pe, pb = prev if prev is not None else (0, 0, None)
     cs, ce, cb = cur
     return _call_with_failures(
@@ -161,7 +161,7 @@ def scan_window(prev: tuple[int, int, np.ndarray] | None,
 
 
 def scan_exponents(prev, cur, k_max: int) -> np.ndarray:
-    """search.py:436-460."""
+    """search.py:255-279."""
     ps, pe, pb = prev if prev is not None else (0, 0, None)
     cs, ce, cb = cur
     out = np.zeros((ce - cs) // 2, dtype=np.uint8)
@@ -173,7 +173,7 @@ def scan_exponents(prev, cur, k_max: int) -> np.ndarray:
 
 def verify(start: int, end: int, *, width: int = 1 << 30, k_max: int | None = None,
            block_slots: int = 1 << 20, threads: int = 1) -> dict:
-    """runner.py:583-633 merged segment-loop summary of [start, end) (end
+    """runner.py:216-252 merged segment-loop summary of [start, end) (end
     normalised as runner.py:57-61), before the k <= 63 failure recheck."""
     if (end - start) % 2:
         end += 1
@@ -191,9 +191,9 @@ def odd_count(start: int, end: int) -> int:
 
 def verify_report(start: int, end: int, *, width: int = 1 << 30, k_max: int | None = None,
                   threads: int = 1) -> dict:
-    """runner.py:549-659 for a complete run without checkpoint: the merged
+    """runner.py:172-282 for a complete run without checkpoint: the merged
     segment summary, failures rechecked to k <= 63 and folded into the
-    histogram (runner.py:494-513, 639-653), records finalised for runs from 1
+    histogram (runner.py:117-136, 258-276), records finalised for runs from 1
     (aggregate.py:121-143).  Returns report_dict's fields (aggregate.py:306-322)
     plus record_candidates."""
     if (end - start) % 2:

@@ -3,7 +3,7 @@
 There is no CPU fallback: if the in-tree library is missing, or no CUDA
 device is visible, every hot-path call raises.  Errors cross the C ABI as
 negative codes and are mapped here onto the exceptions the reference raises
-(ValueError for bad arguments, sieve.py:120-128 / search.py:414-417 style).
+(ValueError for bad arguments, sieve.py:80-88 / search.py:233-236 style).
 """
 
 from __future__ import annotations
@@ -15,7 +15,9 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libsqf2k_b200.so"
+# SQF2K_LIB: an alternative build of the same library (debug / checks
+# variants, tools/build_exp.sh); default the in-tree build
+LIB_PATH = Path(os.environ.get("SQF2K_LIB") or Path(__file__).resolve().parent / "libsqf2k_b200.so")
 
 HIST_LEN = 65
 NONE = (1 << 64) - 1

@@ -46,7 +46,7 @@ __device__ inline void append_n(unsigned long long *list, unsigned long long *co
     if (i < cap) list[i] = n;
 }
 
-// Escalation (search.py:349-397 for k > the tile depth): every listed n
+// Escalation (search.py:168-216 for k > the tile depth): every listed n
 // tries k = k_from..k_max exactly; warp `warp` of `n_warps` takes every
 // n_warps-th entry.
 __device__ inline void escalate_warps(const unsigned long long *esc, uint64_t count,

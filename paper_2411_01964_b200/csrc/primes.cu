@@ -4,13 +4,13 @@
 //   1. base primes <= isqrt(limit) by one CTA (Eratosthenes in shared memory);
 //   2. segmented odd-only sieve, one CTA per 2^16 odd numbers, bits in shared
 //      memory, per-segment popcount;
-//   3. exclusive scan of the segment counts (CUB) and an in-order compaction.
+//   3. exclusive scan of the segment counts (one CTA, collectives.cuh) and an
+//      in-order compaction.
 // Output index 0 is the prime 2.  Runs once per verify call.
 #include <algorithm>
 #include <cmath>
 
-#include <cub/cub.cuh>
-
+#include "collectives.cuh"
 #include "common.cuh"
 #include "tile.cuh"
 
@@ -138,10 +138,10 @@ __global__ void __launch_bounds__(kSmallThreads) prime_small_kernel(uint64_t lim
     }
     const uint32_t v0 = bits[w0];
     const uint32_t v1 = wpt == 2 ? bits[w0 + 1] : 0u;
-    using Scan = cub::BlockScan<uint32_t, kSmallThreads>;
-    __shared__ typename Scan::TempStorage tmp;
-    uint32_t off, total;
-    Scan(tmp).ExclusiveSum((uint32_t)(__popc(v0) + __popc(v1)), off, total);
+    __shared__ uint32_t sums[kSmallThreads / 32];
+    uint32_t total;
+    uint32_t off = block_exclusive_scan<uint32_t, kSmallThreads>((uint32_t)(__popc(v0) + __popc(v1)),
+                                                                 sums, &total);
     for (uint32_t x = v0; x; x &= x - 1) stage[off++] = 2 * (32 * w0 + __ffs(x) - 1) + 1;
     for (uint32_t x = v1; x; x &= x - 1) stage[off++] = 2 * (32 * w0 + 32 + __ffs(x) - 1) + 1;
     __syncthreads();
@@ -168,15 +168,14 @@ __global__ void __launch_bounds__(1024) base_primes_kernel(uint32_t r, uint32_t 
         __syncthreads();
     }
     // ordered compaction with a block scan over per-thread chunks
-    using Scan = cub::BlockScan<uint32_t, 1024>;
-    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t sums[32];
     const uint32_t last = (r - 1) / 2;  // largest index with 2i+1 <= r
     const uint32_t chunk = (last + blockDim.x) / blockDim.x;
     uint32_t lo = 1 + threadIdx.x * chunk, hi = min(lo + chunk, last + 1);
     uint32_t cnt = 0;
     for (uint32_t i = lo; i < hi; ++i) cnt += !comp[i];
-    uint32_t off;
-    Scan(tmp).ExclusiveSum(cnt, off);
+    uint32_t tot;
+    uint32_t off = block_exclusive_scan<uint32_t, 1024>(cnt, sums, &tot);
     for (uint32_t i = lo; i < hi; ++i)
         if (!comp[i]) base[off++] = 2 * i + 1;
     if (threadIdx.x == blockDim.x - 1) *nbase = off;
@@ -235,9 +234,9 @@ __global__ void __launch_bounds__(kSieveThreads) prime_segment_kernel(
         bits[(uint64_t)blockIdx.x * kSegWords + j] = word;
         cnt += __popc(word);
     }
-    using Red = cub::BlockReduce<uint32_t, kSieveThreads>;
-    __shared__ typename Red::TempStorage rt;
-    uint32_t tot = Red(rt).Sum(cnt);
+    __shared__ uint32_t sums[kSieveThreads / 32];
+    uint32_t tot;
+    block_exclusive_scan<uint32_t, kSieveThreads>(cnt, sums, &tot);
     if (threadIdx.x == 0) counts[blockIdx.x] = tot;
 }
 
@@ -254,10 +253,9 @@ __global__ void __launch_bounds__(kSieveThreads) prime_compact_kernel(
         v[j] = w[j];
         cnt += __popc(v[j]);
     }
-    using Scan = cub::BlockScan<uint32_t, kSieveThreads>;
-    __shared__ typename Scan::TempStorage tmp;
-    uint32_t off;
-    Scan(tmp).ExclusiveSum(cnt, off);
+    __shared__ uint32_t sums[kSieveThreads / 32];
+    uint32_t tot;
+    const uint32_t off = block_exclusive_scan<uint32_t, kSieveThreads>(cnt, sums, &tot);
     uint64_t pos = offsets[blockIdx.x] + off + (with_two ? 1 : 0);
     const uint64_t i_base = (uint64_t)blockIdx.x * kSegOdds + (uint64_t)threadIdx.x * kPer * 32;
 #pragma unroll
@@ -333,15 +331,11 @@ void generate_primes_async(uint64_t limit) {
            base, nbase);
     launch("primes_sieve", prime_segment_kernel, dim3((unsigned)nseg), dim3(kSieveThreads), 0,
            limit, (const uint32_t *)base, (const uint32_t *)nbase, bits, counts);
-    // exclusive scan of counts (uint32 in, uint64 out); counts[nseg] = 0 puts
-    // the total in offsets[nseg]
+    // exclusive scan of the nseg segment counts (uint32 in, uint64 out);
+    // offsets[nseg] = the total
     uint64_t *offsets = c.prime_offsets.as<uint64_t>();
-    size_t tmp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, (int)nseg + 1, c.stream);
-    c.scan_tmp.reserve(std::max<size_t>(tmp_bytes, 64));
-    SQF2K_CUDA(cudaMemsetAsync(counts + nseg, 0, 4, c.stream));
-    SQF2K_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.ptr, tmp_bytes, counts, offsets,
-                                             (int)nseg + 1, c.stream));
+    launch("primes_scan", scan_counts_kernel<uint64_t>, dim3(1), dim3(kScanThreads), 0,
+           (const uint32_t *)counts, nseg, offsets);
     launch("primes_compact", prime_compact_kernel, dim3((unsigned)nseg), dim3(kSieveThreads), 0,
            (const uint32_t *)bits, (const uint64_t *)offsets, c.primes_u32.as<uint32_t>(), 1,
            offsets + nseg, info);

@@ -1,6 +1,6 @@
 // scan.cu -- L2 min-k scan over a packed bitmap window in HBM
-// (replaces search.py:400-433 scan_segment and search.py:436-460
-// scan_exponents; window rules of search.py:278-316).
+// (replaces search.py:219-252 scan_segment and search.py:255-279
+// scan_exponents; window rules of search.py:97-135).
 //
 // The window is one device bitmap: zeros | predecessor bits | current bits |
 // zero pad, with current slot 0 at a 128-bit boundary.  One thread owns 128
@@ -456,7 +456,7 @@ unsigned grid_for(uint64_t n_vec) {
         1, std::min<uint64_t>(ceil_div(n_vec, kScanThreads), (uint64_t)c.sm_count * 8));
 }
 
-// Build the device window of search.py:278-316 (validation already done).
+// Build the device window of search.py:97-135 (validation already done).
 // Returns the vector index of current slot 0.
 uint64_t build_window(const uint8_t *prev, uint64_t prev_n, const uint8_t *cur, uint64_t cur_n,
                       uint64_t prev_eff) {
@@ -482,7 +482,7 @@ uint64_t build_window(const uint8_t *prev, uint64_t prev_n, const uint8_t *cur, 
     return P0 / 128;
 }
 
-// Validation of search.py:219-224 and search.py:288-311; returns the
+// Validation of search.py:38-43 and search.py:107-130; returns the
 // effective predecessor depth (slots) or -1 with the error set.
 int64_t window_depth(const uint8_t *prev, uint64_t prev_start, uint64_t prev_end,
                      uint64_t cur_start, uint64_t cur_end, uint32_t k_max) {

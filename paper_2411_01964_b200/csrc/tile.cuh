@@ -2,7 +2,7 @@
 //
 // Domain of one launch ("batch"): slots u in [0, U) standing for the odd
 // integers n(u) = base_n + 2u (base_n odd, possibly <= 0; n < 1 reads as
-// "not squarefree", search.py:282-286).  Tiles are kTile consecutive slots.
+// "not squarefree", search.py:101-105).  Tiles are kTile consecutive slots.
 //
 // Per tile a CTA sieves the tile directly in packed form (one bit per odd
 // slot, 32-bit LSB-first words in shared memory):
@@ -12,7 +12,7 @@
 //      medium primes 11 <= p < kPMed from per-lane "descriptors" whose next
 //      hit offset lives in a register across tiles (no division, no table
 //      walk), bucket primes p >= kPMed from per-tile hit lists in HBM;
-//   3. fused mode: runs the exponent passes k = 1..k_eff of search.py:368-381
+//   3. fused mode: runs the exponent passes k = 1..k_eff of search.py:187-200
 //      over the words -- passes 1..5 unconditionally for every word (funnel
 //      shifts of the word and its left neighbour), the rare remainder
 //      divergently -- reading n - 2^k from the tile or the previous tile's
@@ -34,9 +34,12 @@ namespace sqf2k {
 constexpr int kTileShift = SQF2K_TILE_SHIFT;
 constexpr int kTile = 1 << kTileShift;  // slots per tile (65536)
 constexpr int kTileWords = kTile / 32;  // 2048 packed words
-// bucket lists are kept per 2^16-slot "bucket tile" (16-bit offsets); a tile
-// holds kSubTiles of them
-constexpr int kBucketShift = 16;
+// bucket lists are kept per 2^14-slot "bucket tile" (16-bit offsets) -- the
+// warp tile of warp_tile.cuh; a CTA tile holds kSubTiles of them
+#ifndef SQF2K_BUCKET_SHIFT
+#define SQF2K_BUCKET_SHIFT 14
+#endif
+constexpr int kBucketShift = SQF2K_BUCKET_SHIFT;
 constexpr int kBucketTile = 1 << kBucketShift;
 constexpr int kSubTiles = kTile / kBucketTile;
 static_assert(kTile >= kBucketTile, "tiles are whole bucket tiles");
@@ -94,7 +97,10 @@ constexpr int kStaticEighths = SQF2K_STATIC_EIGHTHS;  // static share of the til
 #endif
 constexpr int kDynMinTiles = SQF2K_DYN_MIN_TILES;  // dynamic balancing from this many tiles per CTA
 constexpr int kResCap = 256;           // deferred residue words per tile
-constexpr int kBucketCap = 64;          // fixed-capacity bucket list per tile (mean ~9)
+// fixed-capacity bucket list per bucket tile (mean <= 2.3 hits per 2^14
+// slots: sum over p >= 1031 of 2^14 / p^2; an overflow reruns the batch with
+// exact lists)
+constexpr int kBucketCap = kBucketShift >= 16 ? 64 : 24;
 constexpr uint32_t kPiBelowPMed = 172;  // pi(1023): table index of the first bucket prime
 constexpr uint32_t kPiSubRoot = 1028;   // pi(8191): last "dense" bucket prime (p^2 < 2^26)
 
@@ -132,6 +138,7 @@ struct TileParams {
                                  // repeated words, so a tile never wraps)
     const uint32_t *med;         // q = p^2 of the medium primes
     const uint2 *tasks;          // [warp][kTaskSlots][lane]: (m | mult << 8, step), step 0 idle
+    const uint2 *wtasks;         // warp tiles: [slot][lane], same encoding, shared by all warps
     const uint32_t *tile_start;  // exact bucket lists: bounds, n_btiles + 1 (or null)
     const uint32_t *tile_count;  // fixed-capacity lists: hits of bucket tile b at b*kBucketCap
     const uint16_t *hits;        // bucket hits, offsets within the bucket tile
@@ -153,6 +160,23 @@ struct TileParams {
     const PrimeInfo *info;
     unsigned int *sched;         // [0] dynamic chunks taken, [1] CTAs done (reset by the last)
 };
+
+// Protocol checks (build with -DSQF2K_CHECKS; tools/checks.sh): ring-buffer
+// ownership tags, barrier phases and index bounds asserted on the device --
+// the in-house substitute for compute-sanitizer's racecheck/synccheck/memcheck,
+// which this pool does not allow.  A failed check prints and traps.
+#ifdef SQF2K_CHECKS
+#define SQF2K_CHECK(cond, ...)                                                   \
+    do {                                                                         \
+        if (!(cond)) {                                                           \
+            printf("SQF2K_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x, #cond);          \
+            __trap();                                                            \
+        }                                                                        \
+    } while (0)
+#else
+#define SQF2K_CHECK(cond, ...) do { } while (0)
+#endif
 
 // residue of the first slot u >= 0 with q | base_n + 2u, i.e. u = -base_n/2 mod q
 __device__ __host__ __forceinline__ uint64_t slot_residue(int64_t base_n, uint64_t q) {
@@ -189,6 +213,10 @@ struct BatchArgs {
     struct Acc *finish_acc;       // non-null: the tile kernel's last CTA finishes the call
     void *finish_host;            //   (escalation + accumulators to this mapped host buffer)
 };
+// the fused pipeline's kernel: warp-independent tiles (warp_tile.cuh) or
+// CTA tiles (tile_kernel); in-tile depth limit of the chosen kernel
+bool warp_tiles();
+uint32_t fused_depth_max();
 void prep_tile_batch(const BatchArgs &a, cudaStream_t st);
 void bucket_batch(const BatchArgs &a, cudaStream_t st);
 void run_tile_batch(const BatchArgs &a);

@@ -2,7 +2,7 @@
 // pipeline), the exact escalation kernel, the failure recheck, the
 // squarefree oracle, and the sieve_segment export entry point.
 //
-// Reference semantics restated (per odd n, search.py:368-397, runner.py:93-102):
+// Reference semantics restated (per odd n, search.py:187-216, runner.py:93-102):
 //   k(n) = min{ k in [1, k_max] : n - 2^k >= 1 and n - 2^k squarefree },
 //   n = 1 excluded, unresolved n are failures; hist[k] counts, min_n[k] keeps
 //   the least n with k(n) = k (record candidates are its suffix minima).
@@ -11,8 +11,7 @@
 #include <cstring>
 #include <vector>
 
-#include <cub/cub.cuh>
-
+#include "collectives.cuh"
 #include "common.cuh"
 #include "finish.cuh"
 #include "tile.cuh"
@@ -66,7 +65,7 @@ __global__ void recheck_kernel(const unsigned long long *__restrict__ ns, uint64
     }
 }
 
-// sieve.py:154-171: trial division by p^2 for every prime p <= isqrt(n)
+// sieve.py:114-131: trial division by p^2 for every prime p <= isqrt(n)
 __global__ void squarefree_kernel(const unsigned long long *__restrict__ ns, uint64_t count,
                                   const uint32_t *__restrict__ primes,
                                   const PrimeInfo *__restrict__ info, uint8_t *__restrict__ out) {
@@ -141,24 +140,31 @@ void finish_summary(sqf2k_summary_t *out, const uint64_t *fail_sorted_head, uint
     out->n_failures = n_fail;
 }
 
-// Sort the device failure list (count <= capacity) and copy to the caller.
+// Sort the device failure list (count <= capacity) and copy to the caller:
+// bitonic sort on the GPU (collectives.cuh), one CTA up to kSortSmem keys.
 int deliver_failures(unsigned long long *fail_dev, uint64_t n_fail, uint64_t *failures,
                      uint64_t fail_cap, uint64_t *smallest) {
     Context &c = ctx();
     *smallest = SQF2K_NONE;
     if (!n_fail) return SQF2K_OK;
-    c.fail_sorted.reserve(n_fail * 8);
-    size_t tmp = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, tmp, fail_dev, c.fail_sorted.as<unsigned long long>(),
-                                   (int)n_fail, 0, 64, c.stream);
-    c.scan_tmp.reserve(std::max<size_t>(tmp, 64));
-    SQF2K_CUDA(cub::DeviceRadixSort::SortKeys(c.scan_tmp.ptr, tmp, fail_dev,
-                                              c.fail_sorted.as<unsigned long long>(), (int)n_fail,
-                                              0, 64, c.stream));
+    uint64_t m = 1;
+    while (m < n_fail) m <<= 1;
+    c.fail_sorted.reserve(m * 8);
+    unsigned long long *keys = c.fail_sorted.as<unsigned long long>();
+    SQF2K_CUDA(cudaMemcpyAsync(keys, fail_dev, n_fail * 8, cudaMemcpyDeviceToDevice, c.stream));
+    if (m <= (uint64_t)kSortSmem) {
+        launch("sort_failures", sort_small_kernel, dim3(1), dim3(kScanThreads), 0, keys,
+               (uint32_t)n_fail);
+    } else {
+        const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(m, 256), 4096);
+        launch("sort_pad", pad_keys_kernel, dim3(grid), dim3(256), 0, keys, n_fail, m);
+        for (uint64_t k = 2; k <= m; k <<= 1)
+            for (uint64_t j = k >> 1; j; j >>= 1)
+                launch("sort_step", bitonic_step_kernel, dim3(grid), dim3(256), 0, keys, m, k, j);
+    }
     uint64_t head = 0;
-    copy_d2h(&head, c.fail_sorted.ptr, 8);
-    if (failures && fail_cap)
-        copy_d2h(failures, c.fail_sorted.ptr, std::min(n_fail, fail_cap) * 8);
+    copy_d2h(&head, keys, 8);
+    if (failures && fail_cap) copy_d2h(failures, keys, std::min(n_fail, fail_cap) * 8);
     SQF2K_CUDA(cudaStreamSynchronize(c.stream));
     *smallest = head;
     return SQF2K_OK;
@@ -169,7 +175,7 @@ int deliver_failures(unsigned long long *fail_dev, uint64_t n_fail, uint64_t *fa
 struct VerifyPlan {
     uint64_t start, end, n_slots, batch, limit, esc_cap, dev_fail_cap;
     uint32_t k_max, k_eff, H, pipeline;
-    bool exact;
+    bool exact, default_depth;
     SmallSet small;
 };
 
@@ -244,8 +250,7 @@ void enqueue_verify(const VerifyPlan &pl) {
     join_side();
     // one fused batch at the default depth: the tile kernel's last CTA does
     // the (rare) escalations and writes the accumulators to pinned memory
-    const bool finish_in_tile = pl.pipeline == 0 && pl.n_slots <= pl.batch &&
-                                pl.k_eff >= (uint32_t)kDepthDefault;
+    const bool finish_in_tile = pl.pipeline == 0 && pl.n_slots <= pl.batch && pl.default_depth;
     // several fused batches with fixed-capacity lists: batch b's pattern and
     // bucket lists are built on the side stream (buffer set b & 1) while batch
     // b - 1's tile kernel runs on the main stream (its tail frees the SMs)
@@ -315,7 +320,8 @@ void plan_key(const VerifyPlan &pl, uint64_t key[8]) {
     key[0] = pl.start;
     key[1] = pl.end;
     key[2] = pl.k_max | ((uint64_t)pl.k_eff << 8) | ((uint64_t)pl.pipeline << 16) |
-             ((uint64_t)pl.exact << 24);
+             ((uint64_t)pl.exact << 24) | ((uint64_t)pl.default_depth << 32) |
+             ((uint64_t)warp_tiles() << 33);
     key[3] = pl.batch;
     key[4] = pl.esc_cap;
     key[5] = pl.dev_fail_cap;
@@ -376,14 +382,18 @@ void capture_graph(const VerifyPlan &pl, const uint64_t key[8]) {
 int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verify_opts_t &o,
                  sqf2k_summary_t *out, uint64_t *failures, uint64_t fail_cap) {
     Context &c = ctx();
-    const uint32_t depth = o.tile_depth ? o.tile_depth : kDepthDefault;
-    if (depth < 1 || depth > (uint32_t)kDepthMax)
+    if (o.tile_depth > (uint32_t)kDepthMax)
         return fail(SQF2K_EINVAL, "tile_depth must be in 1..%d", kDepthMax);
+    // the fused kernel resolves exponents up to its own limit in-tile (warp
+    // tiles: 15); deeper ones are escalated exactly -- results are identical
+    const uint32_t depth_cap = o.pipeline == 0 ? fused_depth_max() : (uint32_t)kDepthMax;
+    const uint32_t depth = std::min(o.tile_depth ? o.tile_depth : (uint32_t)kDepthDefault, depth_cap);
     VerifyPlan pl;
     pl.start = start;
     pl.end = end;
     pl.k_max = k_max;
     pl.k_eff = std::min(k_max, depth);
+    pl.default_depth = o.tile_depth == 0;
     pl.H = std::max<uint32_t>(1024u, 1u << (pl.k_eff - 1));
     if (o.batch_slots > kMaxBatch)
         return fail(SQF2K_EINVAL, "batch_slots must be at most 2^40, got %llu",
@@ -466,7 +476,7 @@ int sieve_bits(uint64_t start, uint64_t end, const int64_t *primes_h, uint64_t n
                uint8_t *out, uint64_t nbytes) {
     Context &c = ctx();
     const uint64_t n_slots = (end - start) / 2;
-    // only primes with p^2 <= end - 1 can clear a slot (sieve.py:137)
+    // only primes with p^2 <= end - 1 can clear a slot (sieve.py:97)
     const uint64_t root = isqrt_u64(end - 1);
     const uint64_t np = std::upper_bound(primes_h, primes_h + n_primes_h, (int64_t)root) - primes_h;
     c.host_primes.reserve(std::max<uint64_t>(np, 1) * 8);

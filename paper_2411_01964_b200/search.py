@@ -7,7 +7,7 @@ consecutive odd n are the window bits shifted by 2^(k-1) slots, read with
 funnel shifts (k <= 8) or aligned 128-bit loads (k >= 9).  The block plan
 and worker count of the reference only partition the work, so they are
 validated and otherwise ignored: results are identical by the merge law
-(search.py:205-208).
+(search.py:24-27).
 """
 
 from __future__ import annotations
@@ -28,7 +28,7 @@ DEFAULT_BLOCK_SLOTS = 1 << 20
 
 @dataclass(frozen=True)
 class SegmentWindow:
-    """Current segment plus its predecessor (search.py:211-232)."""
+    """Current segment plus its predecessor (search.py:30-51)."""
 
     previous: Segment | None
     current: Segment
@@ -60,7 +60,7 @@ class SearchOutcome:
 
 
 def smallest_exponent(n: int, window: SegmentWindow, k_max: int) -> SearchOutcome:
-    """Scalar lookup of one n in an already-sieved window (search.py:247-271);
+    """Scalar lookup of one n in an already-sieved window (search.py:66-90);
     a debugging aid that reads window bits, not a compute path."""
     cur = window.current
     if n % 2 == 0 or not (cur.start <= n < cur.end):
@@ -93,7 +93,7 @@ def _window_args(window: SegmentWindow):
 def scan_segment(window: SegmentWindow, k_max: int, *, block_slots: int = DEFAULT_BLOCK_SLOTS,
                  workers: int = 1) -> SegmentSummary:
     """Histogram, k_sum, records candidates and failures of the current
-    segment (search.py:400-433), computed on the GPU."""
+    segment (search.py:219-252), computed on the GPU."""
     if k_max < 1:
         raise ValueError(f"k_max must be positive, got {k_max}")
     if block_slots < 64 or block_slots % 64:
@@ -117,7 +117,7 @@ def scan_segment(window: SegmentWindow, k_max: int, *, block_slots: int = DEFAUL
 
 def scan_exponents(window: SegmentWindow, k_max: int) -> np.ndarray:
     """Per-slot smallest exponents of the current segment, 0 when unresolved
-    or n = 1 (search.py:436-460), computed on the GPU."""
+    or n = 1 (search.py:255-279), computed on the GPU."""
     if k_max < 1:
         raise ValueError(f"k_max must be positive, got {k_max}")
     pb, ps, pe, cb, cs, ce = _window_args(window)

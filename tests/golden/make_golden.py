@@ -139,17 +139,17 @@ def quick(P, S, Q, A, R) -> dict:
     add_scan("low_2^15_k14_b256", low(1 << 15), 14, block_slots=1 << 8)
     add_scan("low_2048_k10", low(2048), 10)
     add_scan("low_256_k1", low(256), 1)
-    for seed in range(4):  # test_search.py:154-167
+    for seed in range(4):  # test_search.py:54-67
         r = random.Random(seed)
         start = r.randrange(1 << 20, 1 << 34) | 1
         w = Q.SegmentWindow(R.seed_predecessor(start, 14, p1m),
                             S.sieve_segment(start, start + (1 << 14), p1m))
         add_scan(f"high_seed{seed}_k14", w, 14)
-    # shallow predecessor reaching 1, unaligned (search.py:301-306)
+    # shallow predecessor reaching 1, unaligned (search.py:120-125)
     for cs in [65, 101, 1001]:
         w = Q.SegmentWindow(S.sieve_segment(1, cs, p5), S.sieve_segment(cs, cs + 4000, p5))
         add_scan(f"shallow_prev_{cs}_k12", w, 12)
-    # start=2^20+1 with k_max=8 predecessor (test_search.py:219-224)
+    # start=2^20+1 with k_max=8 predecessor (test_search.py:118-123)
     start = (1 << 20) + 1
     w = Q.SegmentWindow(R.seed_predecessor(start, 8, p5),
                         S.sieve_segment(start, start + (1 << 14), p5))

@@ -89,9 +89,9 @@ def test_scan_known_answers():
     cur = (1, 2049, O.sieve_bits(1, 2049, p, 10**5))
     kv = O.scan_exponents(None, cur, 10)
     for n, k in [(3, 1), (5, 1), (11, 2), (29, 3), (533, 4), (849, 5), (127, 2)]:
-        assert kv[(n - 1) // 2] == k, n  # test_search.py:126-132
+        assert kv[(n - 1) // 2] == k, n  # test_search.py:26-32
     cur = (1, (1 << 14) + 1, O.sieve_bits(1, (1 << 14) + 1, p, 10**5))
-    s = O.scan_window(None, cur, 13)  # test_search.py:170-179
+    s = O.scan_window(None, cur, 13)  # test_search.py:70-79
     assert sum(s["histogram"]) == 8191 and s["failures"] == []
     assert [s["record_candidates"][m] for m in (1, 2, 3, 4)] == [11, 29, 533, 849]
 
