@@ -10,6 +10,7 @@
 // per-k least n goes through a block-level atomicMin, failures (or, in the
 // two-pass verify pipeline, escalations) are appended to a device list.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -54,9 +55,6 @@ struct ScanParams {
 // derives it from `scanned` by conservation, as for the fused kernel.
 constexpr int kFastThreads = 256;
 constexpr int kGroupWords = 8;
-#ifndef SQF2K_TMA_SCAN
-#define SQF2K_TMA_SCAN 0
-#endif
 
 // Pending mask of the word starting at slot a (end of range, n = 1).
 __device__ __forceinline__ uint32_t wscan_mask(const ScanParams &P, uint64_t a) {
@@ -216,12 +214,18 @@ __global__ void __launch_bounds__(kFastThreads) wscan_kernel(const ScanParams P)
     }
 }
 
-#if SQF2K_TMA_SCAN
-// TMA-fed variant: the CTA's contiguous run of groups streams through a
-// kStages-deep ring of 8 KB shared-memory blocks, each filled by one bulk copy
-// (cp.async.bulk global -> shared, completion on an mbarrier) issued by thread
-// 0 kStages - 1 blocks ahead; threads read their group (2 x LDS.128) and the
-// word before it from shared memory.  No per-thread global loads on the path.
+// TMA-fed pending-count scan (the default): the CTA's contiguous run of
+// groups streams through a kStages-deep ring of 8 KB shared-memory blocks,
+// each filled by one bulk copy (cp.async.bulk global -> shared, completion on
+// an mbarrier) issued by thread 0 kStages - 1 blocks ahead -- no per-thread
+// global loads and no prefetch registers on the path.  A thread reads its
+// 8-word group (2 x LDS.128) and the word before it from shared memory and
+// runs passes 1..5 as funnel shifts, counting the slots still *pending*
+// after passes 1..4 (covered-bit popcounts, as tile_kernel does: ~16
+// instructions per 32-slot word instead of ~25).  Groups at the range ends
+// and the groups of the first block that still track per-k least slots take
+// the direct-count path (wscan_group); the leftovers after pass 5 (~2e-4 of
+// the words) go to wscan_residue for k >= 6.
 constexpr int kStages = 4;
 constexpr int kBlockGroups = kFastThreads;                  // groups per block
 constexpr int kBlockWords = kBlockGroups * kGroupWords;     // 2048 words = 8 KB
@@ -229,6 +233,35 @@ constexpr int kStageWords = kBlockWords + 4;                // + 16 B: the word 
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+
+// Passes 1..5 of one group by pending counts: p[k] -= covered(k) per word
+// (+ 32 per word added by the caller); returns the words with slots left.
+__device__ __forceinline__ uint32_t wscan_pc_group(const uint32_t (&cur)[kGroupWords], uint32_t prv,
+                                                   uint32_t (&p)[5]) {
+    uint32_t all = ~0u;
+#pragma unroll
+    for (int i = 0; i < kGroupWords; ++i) {
+        const uint32_t cu = cur[i];
+        const uint32_t v1 = __funnelshift_l(prv, cu, 1);
+        const uint32_t v2 = v1 | __funnelshift_l(prv, cu, 2);
+        const uint32_t v3 = v2 | __funnelshift_l(prv, cu, 4);
+        const uint32_t v4 = v3 | __funnelshift_l(prv, cu, 8);
+        const uint32_t v5 = v4 | __funnelshift_l(prv, cu, 16);
+        p[1] -= __popc(v1);
+        p[2] -= __popc(v2);
+        p[3] -= __popc(v3);
+        p[4] -= __popc(v4);
+        all &= v5;
+        prv = cu;
+    }
+    return all;
 }
 
 template <int KMAIN>
@@ -269,9 +302,12 @@ __global__ void __launch_bounds__(kFastThreads) wscan_tma_kernel(const ScanParam
     };
     if (threadIdx.x == 0)
         for (uint64_t j = 0; j < kStages - 1 && j < n_blocks; ++j) issue(j);
-    uint32_t c[6] = {0, 0, 0, 0, 0, 0};
+    uint32_t c[6] = {0, 0, 0, 0, 0, 0};  // direct counts (edge / tracking groups)
+    uint32_t p[5] = {0, 0, 0, 0, 0};     // pending after pass k (pending-count groups)
+    uint32_t left5 = 0;                  // their slots left after pass 5
     unsigned long long scanned = 0;
-    uint32_t tneed = (2u << KMAIN) - 2u;  // k = 1..KMAIN not met yet by this thread
+    const uint32_t all_k = (2u << KMAIN) - 2u;
+    uint32_t need = all_k;  // k = 1..KMAIN whose least slot this CTA has not met
     const uint64_t g_edge = P.n_slots / (32 * kGroupWords);  // groups >= this touch the end
     const uint64_t g_one = P.one_slot == ~0ull ? ~0ull : P.one_slot / (32 * kGroupWords);
     for (uint64_t j = 0; j < n_blocks; ++j) {
@@ -300,21 +336,51 @@ __global__ void __launch_bounds__(kFastThreads) wscan_tma_kernel(const ScanParam
                 cur[4 * v + 3] = x.w;
             }
             const uint32_t prv = b[-1];
-            if (g >= g_edge || g == g_one)
+            uint32_t tneed = need;
+            if (g >= g_edge || g == g_one) {
                 wscan_group<KMAIN, true, true>(P, w, g, word0, cur, prv, c, scanned, tneed, s_cnt, s_first);
-            else if (tneed)
-                wscan_group<KMAIN, true, false>(P, w, g, word0, cur, prv, c, scanned, tneed, s_cnt, s_first);
-            else
-                wscan_group<KMAIN, false, false>(P, w, g, word0, cur, prv, c, scanned, tneed, s_cnt, s_first);
+            } else if (KMAIN < 5 || need) {
+                if (need) wscan_group<KMAIN, true, false>(P, w, g, word0, cur, prv, c, scanned, tneed, s_cnt, s_first);
+                else wscan_group<KMAIN, false, false>(P, w, g, word0, cur, prv, c, scanned, tneed, s_cnt, s_first);
+            } else {
+                const uint32_t all = wscan_pc_group(cur, prv, p);
+#pragma unroll
+                for (int k = 1; k <= 4; ++k) p[k] += 32 * kGroupWords;
+                scanned += 32 * kGroupWords;
+                if (all != ~0u) {  // rare: some slots left after pass 5
+                    uint32_t pv = prv;
+                    const uint64_t wg = word0 + g * kGroupWords, s0 = g * 32 * kGroupWords;
+#pragma unroll
+                    for (int i = 0; i < kGroupWords; ++i) {
+                        const uint32_t cu = cur[i];
+                        const uint32_t v5 = __funnelshift_l(pv, cu, 1) | __funnelshift_l(pv, cu, 2) |
+                                            __funnelshift_l(pv, cu, 4) | __funnelshift_l(pv, cu, 8) |
+                                            __funnelshift_l(pv, cu, 16);
+                        pv = cu;
+                        if (v5 == ~0u) continue;
+                        left5 += __popc(~v5);
+                        wscan_residue(P, w, wg + i, s0 + 32 * i, 5, s_cnt, s_first);
+                    }
+                }
+            }
         }
         __syncthreads();  // stage st may be refilled (block j + kStages) from here on
+        if (need) {       // least slots met in this block end the tracking (later blocks are larger)
+            uint32_t nn = 0;
+#pragma unroll
+            for (int k = 1; k <= KMAIN; ++k)
+                if (s_first[k] == ~0ull) nn |= 1u << k;
+            need = nn & all_k;
+        }
     }
 #pragma unroll
-    for (int k = 2; k <= 5; ++k) {
-        const uint32_t s = __reduce_add_sync(0xffffffffu, c[k]);
-        if ((threadIdx.x & 31) == 0 && s) atomicAdd(&s_cnt[k], s);
+    for (int k = 2; k <= 5; ++k) {  // direct counts, then the pending differences
+        unsigned long long v = c[k];
+        if (KMAIN == 5) v += (k < 5 ? (unsigned long long)(p[k - 1] - p[k]) : (unsigned long long)(p[4] - left5));
+        const unsigned long long s = warp_sum64(v);
+        if ((threadIdx.x & 31) == 0 && s) atomicAdd(&P.hist[k], s);
     }
-    for (int d = 16; d >= 1; d >>= 1) scanned += __shfl_xor_sync(0xffffffffu, scanned, d);
+    scanned = warp_sum64(scanned);
     if ((threadIdx.x & 31) == 0 && scanned) atomicAdd(P.scanned, scanned);
     __syncthreads();
     for (int k = threadIdx.x; k < 65; k += blockDim.x) {
@@ -324,7 +390,6 @@ __global__ void __launch_bounds__(kFastThreads) wscan_tma_kernel(const ScanParam
     }
 }
 
-#endif  // SQF2K_TMA_SCAN
 
 template <bool EXPO>
 __global__ void __launch_bounds__(kScanThreads) window_scan_kernel(const ScanParams P) {
@@ -546,23 +611,28 @@ void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_sl
     const uint64_t groups = ceil_div(n_slots, 32 * kGroupWords);
     const unsigned grid = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>(ceil_div(groups, kFastThreads), (uint64_t)ctx().sm_count * 8));
-#if SQF2K_TMA_SCAN
-    const size_t smem = (size_t)kStages * kStageWords * 4;
-    static bool attr = false;
-    if (!attr) {
-        for (auto *k : {wscan_tma_kernel<1>, wscan_tma_kernel<2>, wscan_tma_kernel<3>,
-                        wscan_tma_kernel<4>, wscan_tma_kernel<5>})
-            SQF2K_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+    static const bool ldg = [] {  // SQF2K_SCAN_KERNEL=ldg: the register-pipelined kernel (A/B)
+        const char *e = std::getenv("SQF2K_SCAN_KERNEL");
+        return e && std::strcmp(e, "ldg") == 0;
+    }();
+    if (!ldg) {
+        const size_t smem = (size_t)kStages * kStageWords * 4;
+        static bool attr = false;
+        if (!attr) {
+            for (auto *k : {wscan_tma_kernel<1>, wscan_tma_kernel<2>, wscan_tma_kernel<3>,
+                            wscan_tma_kernel<4>, wscan_tma_kernel<5>})
+                SQF2K_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        switch (std::min<uint32_t>(k_scan, 5)) {
+            case 1: launch("window_scan", wscan_tma_kernel<1>, dim3(grid), dim3(kFastThreads), smem, P); break;
+            case 2: launch("window_scan", wscan_tma_kernel<2>, dim3(grid), dim3(kFastThreads), smem, P); break;
+            case 3: launch("window_scan", wscan_tma_kernel<3>, dim3(grid), dim3(kFastThreads), smem, P); break;
+            case 4: launch("window_scan", wscan_tma_kernel<4>, dim3(grid), dim3(kFastThreads), smem, P); break;
+            default: launch("window_scan", wscan_tma_kernel<5>, dim3(grid), dim3(kFastThreads), smem, P); break;
+        }
+        return;
     }
-    switch (std::min<uint32_t>(k_scan, 5)) {
-        case 1: launch("window_scan", wscan_tma_kernel<1>, dim3(grid), dim3(kFastThreads), smem, P); break;
-        case 2: launch("window_scan", wscan_tma_kernel<2>, dim3(grid), dim3(kFastThreads), smem, P); break;
-        case 3: launch("window_scan", wscan_tma_kernel<3>, dim3(grid), dim3(kFastThreads), smem, P); break;
-        case 4: launch("window_scan", wscan_tma_kernel<4>, dim3(grid), dim3(kFastThreads), smem, P); break;
-        default: launch("window_scan", wscan_tma_kernel<5>, dim3(grid), dim3(kFastThreads), smem, P); break;
-    }
-#else
     switch (std::min<uint32_t>(k_scan, 5)) {
         case 1: launch("window_scan", wscan_kernel<1>, dim3(grid), dim3(kFastThreads), 0, P); break;
         case 2: launch("window_scan", wscan_kernel<2>, dim3(grid), dim3(kFastThreads), 0, P); break;
@@ -570,7 +640,6 @@ void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_sl
         case 4: launch("window_scan", wscan_kernel<4>, dim3(grid), dim3(kFastThreads), 0, P); break;
         default: launch("window_scan", wscan_kernel<5>, dim3(grid), dim3(kFastThreads), 0, P); break;
     }
-#endif
 }
 
 }  // namespace sqf2k

@@ -305,27 +305,27 @@ __device__ __forceinline__ void init_medium(MedLane &L, const TileParams &P, uin
 }
 
 // clear the bucket hits of tile t with offsets in [skip, kTile), shifted by
-// -skip: its kSubTiles bucket-tile lists, one list per warp on the last
-// kSubTiles warps (~2.3 hits per 2^14-slot list; build_med gives those warps
-// less medium work)
+// -skip (its kSubTiles bucket-tile lists); run by the last warp only (~9
+// hits per 2^16 slots; build_med gives that warp less medium work)
 __device__ __forceinline__ void scatter_bucket(uint32_t wbase, const TileParams &P, uint32_t t,
                                                uint32_t skip) {
-    static_assert(kSubTiles <= kThreads / 32, "a warp per bucket list");
-    const int j = (int)(threadIdx.x >> 5) - (kThreads / 32 - kSubTiles);
-    if (j < 0) return;
-    const uint32_t bt = t * kSubTiles + j;
-    if (bt >= P.n_btiles || (uint32_t)(j + 1) * kBucketTile <= skip) return;
-    uint32_t b, e;
-    if (P.tile_start) {
-        b = __ldg(&P.tile_start[bt]);
-        e = __ldg(&P.tile_start[bt + 1]);
-    } else {
-        b = bt * (uint32_t)kBucketCap;
-        e = b + min(__ldg(&P.tile_count[bt]), (uint32_t)kBucketCap);
-    }
-    for (uint32_t i = b + (threadIdx.x & 31); i < e; i += 32) {
-        const uint32_t o = j * kBucketTile + __ldg(&P.hits[i]);
-        if (o >= skip) clear_bit(wbase, o - skip);
+    if ((threadIdx.x >> 5) != kThreads / 32 - 1) return;
+#pragma unroll
+    for (int j = 0; j < kSubTiles; ++j) {
+        const uint32_t bt = t * kSubTiles + j;
+        if (bt >= P.n_btiles || (uint32_t)(j + 1) * kBucketTile <= skip) continue;
+        uint32_t b, e;
+        if (P.tile_start) {
+            b = __ldg(&P.tile_start[bt]);
+            e = __ldg(&P.tile_start[bt + 1]);
+        } else {
+            b = bt * (uint32_t)kBucketCap;
+            e = b + min(__ldg(&P.tile_count[bt]), (uint32_t)kBucketCap);
+        }
+        for (uint32_t i = b + (threadIdx.x & 31); i < e; i += 32) {
+            const uint32_t o = j * kBucketTile + __ldg(&P.hits[i]);
+            if (o >= skip) clear_bit(wbase, o - skip);
+        }
     }
 }
 
@@ -983,8 +983,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     TL(3);
 }
 
-#include "warp_tile.cuh"
-
 // -------------------------------------------------------------------------
 // Medium-prime scatter schedule, built on the host from the table's primes in
 // [11, kPMed) and cached on the device per set.  A prime with h = kTile/q
@@ -1030,8 +1028,7 @@ MedTables build_med(const std::vector<uint32_t> &med_primes) {
         const uint32_t n_tasks = (uint32_t)((descs.size() + 31) / 32);
         if (n_tasks > (uint32_t)(kWarps * kTaskSlots)) continue;
         std::vector<double> load(kWarps, 0.0);
-        for (int j = 0; j < kSubTiles; ++j)  // the bucket warps (scatter_bucket)
-            load[kWarps - 1 - j] = SQF2K_LPT_BUCKET / kSubTiles;
+        load[kWarps - 1] = SQF2K_LPT_BUCKET;  // the bucket warp (scatter_bucket)
         std::vector<int> used(kWarps, 0);
         t.tasks.assign((size_t)kWarps * kTaskSlots * 64, 0u);  // step 0: idle lane
         for (uint32_t k = 0; k < n_tasks; ++k) {  // longest first, least-loaded warp with room
@@ -1056,53 +1053,10 @@ MedTables build_med(const std::vector<uint32_t> &med_primes) {
 
 struct MedCache {
     std::vector<uint32_t> key;
-    DevBuf buf;  // kMaxMed q values, then the task table, then the warp-tile table
+    DevBuf buf;  // kMaxMed q values, then the task table
 };
 
 MedCache g_med;  // the library serialises calls
-
-// Warp-tile schedule: one table [kWtSlots][32 lanes] shared by every warp
-// (each warp sieves its own tiles with all medium primes).  A prime with
-// h = kWt / q hits per tile is split into parts = ceil(h / item) descriptors
-// (start multiple j, step parts * q) of <= item hits; descriptors sorted by
-// trip count fill the slots slot-major, so the 32 lanes of a slot run loops
-// of nearly equal length.  A slot costs its longest lane (plus loop exit),
-// so the item size is chosen to minimise the sum over slots of the maximum
-// trip count among the schedules that fit the register slots.
-std::vector<uint32_t> build_wmed(const std::vector<uint32_t> &med_primes) {
-    struct Desc {
-        double trips;
-        uint32_t x, y;
-    };
-    std::vector<Desc> best;
-    double best_cost = 1e300;
-    for (double item = 1.0; item <= 64.0; item += 0.25) {
-        std::vector<Desc> descs;
-        for (size_t m = 0; m < med_primes.size() && m < (size_t)kMaxMed; ++m) {
-            const uint32_t q = med_primes[m] * med_primes[m];
-            const double h = (double)kWt / q;
-            const uint32_t parts = h > item ? (uint32_t)std::ceil(h / item) : 1u;
-            for (uint32_t j = 0; j < parts; ++j)
-                descs.push_back({h / parts, (uint32_t)m | (j << 8), parts * q});
-        }
-        if (descs.size() > (size_t)kWtSlots * 32) continue;
-        std::stable_sort(descs.begin(), descs.end(),
-                         [](const Desc &a, const Desc &b) { return a.trips > b.trips; });
-        double cost = 0.0;
-        for (size_t i = 0; i < descs.size(); i += 32) cost += descs[i].trips + 0.5;
-        if (cost < best_cost) {
-            best_cost = cost;
-            best = descs;
-        }
-    }
-    if (best.empty()) throw Error{SQF2K_ECUDA, "warp-tile medium schedule does not fit the slots"};
-    std::vector<uint32_t> t((size_t)kWtSlots * 64, 0u);  // step 0: idle lane
-    for (size_t i = 0; i < best.size(); ++i) {
-        t[2 * i] = best[i].x;  // slot i / 32, lane i % 32
-        t[2 * i + 1] = best[i].y;
-    }
-    return t;
-}
 
 }  // namespace
 
@@ -1119,17 +1073,6 @@ std::vector<uint32_t> small_primes(uint32_t below) {
 }
 
 size_t tile_smem_bytes() { return sizeof(TileSmem); }
-
-// SQF2K_FUSED_KERNEL=cta selects the CTA-tile kernel for the fused pipeline
-// (A/B measurements); the default is warp-independent tiles.
-bool warp_tiles() {
-    static const bool on = [] {
-        const char *e = std::getenv("SQF2K_FUSED_KERNEL");
-        return !(e && std::strcmp(e, "cta") == 0);
-    }();
-    return on;
-}
-uint32_t fused_depth_max() { return warp_tiles() ? (uint32_t)kWtDepthMax : (uint32_t)kDepthMax; }
 
 // Upper bound of the bucket hits of a domain of U slots: sum over odd p >= 1031
 // of (U/p^2 + 1) <= U / (2 * 1029) + n_bucket_primes.
@@ -1151,20 +1094,6 @@ void launch_tile(const char *name, unsigned grid, size_t smem, const TileParams 
     launch_pdl(name, tile_kernel<FUSED, KMAIN>, dim3(grid), dim3(kThreads), smem, P);
 }
 
-template <int KMAIN>
-void launch_wtile(unsigned grid, size_t smem, const TileParams &P) {
-    static bool attr = false;
-    if (!attr) {
-        SQF2K_CUDA(cudaFuncSetAttribute(wtile_kernel<KMAIN>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const int pct = (int)((kWtCtasPerSm * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
-        SQF2K_CUDA(cudaFuncSetAttribute(wtile_kernel<KMAIN>,
-                                        cudaFuncAttributePreferredSharedMemoryCarveout, std::min(pct, 100)));
-        attr = true;
-    }
-    launch_pdl("tile_fused", wtile_kernel<KMAIN>, dim3(grid), dim3(kWtThreads), smem, P);
-}
-
 // Work of a batch that does not need the prime table: the medium schedule
 // (host-built, cached), the p = 3, 5, 7 pattern and the bucket counters --
 // on stream `st` (the side stream for the first batch of a call).
@@ -1173,16 +1102,13 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
 
     // medium tables: cached per distinct prime set
     constexpr size_t kTaskWords = (size_t)(kThreads / 32) * kTaskSlots * 64;
-    constexpr size_t kWTaskWords = (size_t)kWtSlots * 64;
     if (g_med.key != *a.med_primes || !g_med.buf.ptr) {
         MedTables t = build_med(*a.med_primes);
-        const std::vector<uint32_t> wt = build_wmed(*a.med_primes);
         g_med.key = *a.med_primes;
-        g_med.buf.reserve((kMaxMed + kTaskWords + kWTaskWords) * 4);
-        std::vector<uint32_t> host(kMaxMed + kTaskWords + kWTaskWords, 0);
+        g_med.buf.reserve((kMaxMed + kTaskWords) * 4);
+        std::vector<uint32_t> host(kMaxMed + kTaskWords, 0);
         std::copy(t.q.begin(), t.q.end(), host.begin());
         std::copy(t.tasks.begin(), t.tasks.end(), host.begin() + kMaxMed);
-        std::copy(wt.begin(), wt.end(), host.begin() + kMaxMed + kTaskWords);
         SQF2K_CUDA(cudaMemcpy(g_med.buf.ptr, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
         dev_alloc_bump();  // captured graphs read this table
     }
@@ -1300,24 +1226,6 @@ void run_tile_batch(const BatchArgs &a) {
     P.primes = a.primes;
     P.info = a.info;
 
-    P.wtasks = reinterpret_cast<const uint2 *>(g_med.buf.as<uint32_t>() + kMaxMed +
-                                               (size_t)(kThreads / 32) * kTaskSlots * 64);
-    if (a.fused && warp_tiles()) {
-        P.n_tiles = (uint32_t)ceil_div(a.U, kWt);
-        const size_t smem = sizeof(WtSmem);
-        uint64_t grid_cap = (uint64_t)c.sm_count * kWtCtasPerSm;
-        if (const char *g = std::getenv("SQF2K_DEBUG_GRID")) grid_cap = std::max(1, atoi(g));
-        grid_cap = std::max<uint64_t>(grid_cap, ceil_div(P.n_tiles, (1ull << 23) * kWtWarps));
-        const unsigned grid = (unsigned)std::max<uint64_t>(
-            1, std::min<uint64_t>(ceil_div(P.n_tiles, kWtWarps), grid_cap));
-        const uint32_t kmain = std::min<uint32_t>(a.k_eff, kMainMax);
-        if (kmain == 1) launch_wtile<1>(grid, smem, P);
-        else if (kmain == 2) launch_wtile<2>(grid, smem, P);
-        else if (kmain == 3) launch_wtile<3>(grid, smem, P);
-        else if (kmain == 4) launch_wtile<4>(grid, smem, P);
-        else launch_wtile<5>(grid, smem, P);
-        return;
-    }
     const size_t smem = tile_smem_bytes();
     uint64_t grid_cap = (uint64_t)c.sm_count * kCtasPerSm;
     if (const char *g = std::getenv("SQF2K_DEBUG_GRID")) grid_cap = std::max(1, atoi(g));

@@ -34,10 +34,10 @@ namespace sqf2k {
 constexpr int kTileShift = SQF2K_TILE_SHIFT;
 constexpr int kTile = 1 << kTileShift;  // slots per tile (65536)
 constexpr int kTileWords = kTile / 32;  // 2048 packed words
-// bucket lists are kept per 2^14-slot "bucket tile" (16-bit offsets) -- the
-// warp tile of warp_tile.cuh; a CTA tile holds kSubTiles of them
+// bucket lists are kept per "bucket tile" of 2^kBucketShift slots (16-bit
+// offsets); a tile holds kSubTiles of them
 #ifndef SQF2K_BUCKET_SHIFT
-#define SQF2K_BUCKET_SHIFT 14
+#define SQF2K_BUCKET_SHIFT 16
 #endif
 constexpr int kBucketShift = SQF2K_BUCKET_SHIFT;
 constexpr int kBucketTile = 1 << kBucketShift;
@@ -97,8 +97,8 @@ constexpr int kStaticEighths = SQF2K_STATIC_EIGHTHS;  // static share of the til
 #endif
 constexpr int kDynMinTiles = SQF2K_DYN_MIN_TILES;  // dynamic balancing from this many tiles per CTA
 constexpr int kResCap = 256;           // deferred residue words per tile
-// fixed-capacity bucket list per bucket tile (mean <= 2.3 hits per 2^14
-// slots: sum over p >= 1031 of 2^14 / p^2; an overflow reruns the batch with
+// fixed-capacity bucket list per bucket tile (mean <= 9.2 hits per 2^16
+// slots: sum over p >= 1031 of 2^16 / p^2; an overflow reruns the batch with
 // exact lists)
 constexpr int kBucketCap = kBucketShift >= 16 ? 64 : 24;
 constexpr uint32_t kPiBelowPMed = 172;  // pi(1023): table index of the first bucket prime
@@ -138,7 +138,6 @@ struct TileParams {
                                  // repeated words, so a tile never wraps)
     const uint32_t *med;         // q = p^2 of the medium primes
     const uint2 *tasks;          // [warp][kTaskSlots][lane]: (m | mult << 8, step), step 0 idle
-    const uint2 *wtasks;         // warp tiles: [slot][lane], same encoding, shared by all warps
     const uint32_t *tile_start;  // exact bucket lists: bounds, n_btiles + 1 (or null)
     const uint32_t *tile_count;  // fixed-capacity lists: hits of bucket tile b at b*kBucketCap
     const uint16_t *hits;        // bucket hits, offsets within the bucket tile
@@ -213,10 +212,6 @@ struct BatchArgs {
     struct Acc *finish_acc;       // non-null: the tile kernel's last CTA finishes the call
     void *finish_host;            //   (escalation + accumulators to this mapped host buffer)
 };
-// the fused pipeline's kernel: warp-independent tiles (warp_tile.cuh) or
-// CTA tiles (tile_kernel); in-tile depth limit of the chosen kernel
-bool warp_tiles();
-uint32_t fused_depth_max();
 void prep_tile_batch(const BatchArgs &a, cudaStream_t st);
 void bucket_batch(const BatchArgs &a, cudaStream_t st);
 void run_tile_batch(const BatchArgs &a);

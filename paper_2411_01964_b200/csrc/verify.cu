@@ -320,8 +320,7 @@ void plan_key(const VerifyPlan &pl, uint64_t key[8]) {
     key[0] = pl.start;
     key[1] = pl.end;
     key[2] = pl.k_max | ((uint64_t)pl.k_eff << 8) | ((uint64_t)pl.pipeline << 16) |
-             ((uint64_t)pl.exact << 24) | ((uint64_t)pl.default_depth << 32) |
-             ((uint64_t)warp_tiles() << 33);
+             ((uint64_t)pl.exact << 24) | ((uint64_t)pl.default_depth << 32);
     key[3] = pl.batch;
     key[4] = pl.esc_cap;
     key[5] = pl.dev_fail_cap;
@@ -384,10 +383,7 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
     Context &c = ctx();
     if (o.tile_depth > (uint32_t)kDepthMax)
         return fail(SQF2K_EINVAL, "tile_depth must be in 1..%d", kDepthMax);
-    // the fused kernel resolves exponents up to its own limit in-tile (warp
-    // tiles: 15); deeper ones are escalated exactly -- results are identical
-    const uint32_t depth_cap = o.pipeline == 0 ? fused_depth_max() : (uint32_t)kDepthMax;
-    const uint32_t depth = std::min(o.tile_depth ? o.tile_depth : (uint32_t)kDepthDefault, depth_cap);
+    const uint32_t depth = o.tile_depth ? o.tile_depth : (uint32_t)kDepthDefault;
     VerifyPlan pl;
     pl.start = start;
     pl.end = end;
@@ -395,9 +391,6 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
     pl.k_eff = std::min(k_max, depth);
     pl.default_depth = o.tile_depth == 0;
     pl.H = std::max<uint32_t>(1024u, 1u << (pl.k_eff - 1));
-    if (o.batch_slots > kMaxBatch)
-        return fail(SQF2K_EINVAL, "batch_slots must be at most 2^40, got %llu",
-                    (unsigned long long)o.batch_slots);
     pl.batch = std::max<uint64_t>(o.batch_slots ? o.batch_slots : kDefaultBatch, (uint64_t)kTile);
     pl.n_slots = (end - start) / 2;
     pl.limit = isqrt_u64(end - 1);
@@ -601,6 +594,11 @@ extern "C" int sqf2k_verify(uint64_t start, uint64_t end, uint32_t k_max,
     std::memset(&o, 0, sizeof o);
     if (opts) o = *opts;
     if (o.pipeline > 1) return fail(SQF2K_EINVAL, "unknown pipeline %u", o.pipeline);
+    if (o.batch_slots > kMaxBatch)
+        return fail(SQF2K_EINVAL, "batch_slots must be at most 2^40, got %llu",
+                    (unsigned long long)o.batch_slots);
+    if (o.tile_depth > (uint32_t)kDepthMax)
+        return fail(SQF2K_EINVAL, "tile_depth must be in 1..%d", kDepthMax);
     return guarded([&](Context &) -> int {
         return verify_range(start, end, k_max, o, out, failures, fail_cap);
     });

@@ -70,3 +70,21 @@ def test_argument_errors_before_device():
     assert lib.sqf2k_verify(3, 10, 3, None, ctypes.byref(s), None, 0) == _lib.EINVAL
     assert lib.sqf2k_verify(1, (1 << 62) + 3, 3, None, ctypes.byref(s), None, 0) == _lib.EINVAL
     assert lib.sqf2k_verify(1, 101, 0, None, ctypes.byref(s), None, 0) == _lib.EINVAL
+    big = _lib.VerifyOpts(0, 0, (1 << 40) + 1, 0, 0)  # batch beyond the 32-bit tile counters' bound
+    assert lib.sqf2k_verify(1, 101, 3, ctypes.byref(big), ctypes.byref(s), None, 0) == _lib.EINVAL
+    assert b"batch_slots" in lib.sqf2k_last_error()
+    deep = _lib.VerifyOpts(0, 17, 0, 0, 0)
+    assert lib.sqf2k_verify(1, 101, 3, ctypes.byref(deep), ctypes.byref(s), None, 0) == _lib.EINVAL
+
+
+def test_run_config_bounds():
+    from paper_2411_01964_b200.runner import ConfigError, RunConfig
+    with pytest.raises(ConfigError, match="batch_slots"):
+        RunConfig(start=1, end=1 << 20, batch_slots=(1 << 40) + 1).validate()
+    with pytest.raises(ConfigError, match="2\\^62"):
+        RunConfig(start=1, end=(1 << 62) + 2).validate()
+    with pytest.raises(ConfigError, match="tile_depth"):
+        RunConfig(start=1, end=1 << 20, tile_depth=17).validate()
+    with pytest.raises(ValueError, match="2\\^32"):
+        from paper_2411_01964_b200.primes import generate_primes
+        generate_primes(1 << 32)

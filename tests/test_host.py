@@ -145,3 +145,24 @@ def test_golden_large_reports_render(golden_large):
         assert render_report_json(rep) == e["report_json"], e["config"]
         doc = json.loads(e["report_json"])
         assert doc["odd_scanned"] == s.odd_scanned
+
+
+def test_checkpoint_writer_keeps_order_and_surfaces_errors(tmp_path):
+    # run_verify's background writer (batch-granular checkpoints): writes land
+    # in submission order, the file holds the last one, errors reach the caller
+    from paper_2411_01964_b200.aggregate import SegmentSummary, VerifyReport, read_checkpoint
+    from paper_2411_01964_b200.runner import _CheckpointWriter
+
+    path = tmp_path / "cp.txt"
+    w = _CheckpointWriter(path)
+    for seq in range(1, 6):
+        w.submit(VerifyReport(start=1, end=1 << 20, segment_width=1 << 16, k_max=16, sequence=seq,
+                              next_start=1 + seq * (1 << 16), elapsed_s=0.0,
+                              summary=SegmentSummary.empty()))
+    w.close()
+    assert read_checkpoint(path).sequence == 5
+    bad = _CheckpointWriter(tmp_path / "missing_dir" / "cp.txt")
+    bad.submit(VerifyReport(start=1, end=3, segment_width=1 << 14, k_max=14, sequence=1,
+                            next_start=3, elapsed_s=0.0, summary=SegmentSummary.empty()))
+    with pytest.raises(OSError):
+        bad.close()
