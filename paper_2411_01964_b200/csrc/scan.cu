@@ -264,8 +264,14 @@ __device__ __forceinline__ uint32_t wscan_pc_group(const uint32_t (&cur)[kGroupW
     return all;
 }
 
+#ifndef SQF2K_SCAN_GRID_PER_SM
+#define SQF2K_SCAN_GRID_PER_SM 32
+#endif
+#ifndef SQF2K_SCAN_MIN_CTAS
+#define SQF2K_SCAN_MIN_CTAS 6
+#endif
 template <int KMAIN>
-__global__ void __launch_bounds__(kFastThreads) wscan_tma_kernel(const ScanParams P) {
+__global__ void __launch_bounds__(kFastThreads, SQF2K_SCAN_MIN_CTAS) wscan_tma_kernel(const ScanParams P) {
     extern __shared__ __align__(128) uint32_t stage[];  // kStages x kStageWords
     __shared__ __align__(8) unsigned long long full[kStages];
     __shared__ unsigned long long s_first[65];
@@ -609,8 +615,16 @@ void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_sl
     P.fail_cap = fail_cap;
     P.scanned = scanned;
     const uint64_t groups = ceil_div(n_slots, 32 * kGroupWords);
-    const unsigned grid = (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>(ceil_div(groups, kFastThreads), (uint64_t)ctx().sm_count * 8));
+    // several waves of CTAs with contiguous runs: CTAs that finish early are
+    // replaced by the next wave's (measured faster than one wave of long runs)
+    // (TMA kernel: 32 CTAs per SM, 3.39 vs 3.08 TB/s at 8; the register-pipelined
+    // kernel prefers 8)
+    static const char *grid_env = std::getenv("SQF2K_SCAN_GRID_PER_SM");  // A/B measurements
+    auto waves = [&](auto, size_t, uint64_t dflt) {
+        const uint64_t per_sm = grid_env ? (uint64_t)std::max(1, atoi(grid_env)) : dflt;
+        return (unsigned)std::max<uint64_t>(
+            1, std::min<uint64_t>(ceil_div(groups, kFastThreads), (uint64_t)ctx().sm_count * per_sm));
+    };
     static const bool ldg = [] {  // SQF2K_SCAN_KERNEL=ldg: the register-pipelined kernel (A/B)
         const char *e = std::getenv("SQF2K_SCAN_KERNEL");
         return e && std::strcmp(e, "ldg") == 0;
@@ -624,6 +638,7 @@ void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_sl
                 SQF2K_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             attr = true;
         }
+        const unsigned grid = waves(wscan_tma_kernel<5>, smem, SQF2K_SCAN_GRID_PER_SM);
         switch (std::min<uint32_t>(k_scan, 5)) {
             case 1: launch("window_scan", wscan_tma_kernel<1>, dim3(grid), dim3(kFastThreads), smem, P); break;
             case 2: launch("window_scan", wscan_tma_kernel<2>, dim3(grid), dim3(kFastThreads), smem, P); break;
@@ -633,6 +648,7 @@ void scan_bitmap_device(const uint32_t *words, uint64_t cur_word0, uint64_t n_sl
         }
         return;
     }
+    const unsigned grid = waves(wscan_kernel<5>, 0, 8);
     switch (std::min<uint32_t>(k_scan, 5)) {
         case 1: launch("window_scan", wscan_kernel<1>, dim3(grid), dim3(kFastThreads), 0, P); break;
         case 2: launch("window_scan", wscan_kernel<2>, dim3(grid), dim3(kFastThreads), 0, P); break;

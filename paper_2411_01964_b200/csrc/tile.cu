@@ -223,6 +223,31 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
 // hint elapses) instead of re-issuing the poll
 constexpr uint32_t kWaitHintNs = SQF2K_WAIT_HINT_NS;
 constexpr uint32_t kWaitSleepNs = SQF2K_WAIT_SLEEP_NS;
+// Named-barrier form of the split phase (SQF2K_NAMED_BAR=1, measured):
+// phase p's barrier is id 1 + (p & 1) with 2 * kThreads arrivals -- every
+// thread arrives (bar.arrive) at the end of phase p and syncs (bar.sync) at
+// its wait in phase p + 1, so waiting warps sleep in hardware instead of
+// polling, at the price of a full barrier at the wait point.  Ids alternate
+// safely: a thread reaches phase p + 2's arrival only after passing phase
+// p + 1's sync, which needs every thread past phase p's sync.
+#ifndef SQF2K_NAMED_BAR
+#define SQF2K_NAMED_BAR 0
+#endif
+__device__ __forceinline__ void phase_arrive(unsigned long long *bar, uint32_t phase) {
+#if SQF2K_NAMED_BAR
+    asm volatile("bar.arrive %0, %1;" ::"r"(1u + (phase & 1u)), "r"(2u * kThreads) : "memory");
+#else
+    mbar_arrive(bar);
+#endif
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity);
+__device__ __forceinline__ void phase_wait(unsigned long long *bar, uint32_t phase) {
+#if SQF2K_NAMED_BAR
+    asm volatile("bar.sync %0, %1;" ::"r"(1u + (phase & 1u)), "r"(2u * kThreads) : "memory");
+#else
+    mbar_wait(bar, phase & 1u);
+#endif
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
     uint32_t done = 0;
     for (;;) {
@@ -905,7 +930,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         uint32_t hb = ring_base(t0), hb1 = ring_base(t0 + 1), hb3 = ring_base(t0 + 3);
         for (uint32_t t = t0; t < t1; ++t) {
             if (t + 1 < t1) sieve_tile(t + 1, hb1);
-            if (t > t0) mbar_wait(&S.mbar, (mbar_phase - 1) & 1u);
+            if (t > t0) phase_wait(&S.mbar, mbar_phase - 1);
 #ifdef SQF2K_CHECKS
             // split phase: every warp has arrived on phase t - 1 and none is
             // more than one phase ahead of this one
@@ -921,14 +946,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             __syncwarp();
             if ((threadIdx.x & 31) == 0) atomicAdd(&S.wphase[threadIdx.x >> 5], 1u);
 #endif
-            mbar_arrive(&S.mbar);
+            phase_arrive(&S.mbar, mbar_phase);
             ++mbar_phase;
             hb = hb1;
             hb1 = next_base(hb1);
             hb3 = next_base(hb3);
             TLT(t - t0);
         }
-        mbar_wait(&S.mbar, (mbar_phase - 1) & 1u);
+        phase_wait(&S.mbar, mbar_phase - 1);
 #endif
         if (FUSED) {  // the chunk's last tile: deferred words and minima
             if (KMAIN == kMainMax) drain_residue(S, P, t1 - 1, S.need);
