@@ -146,8 +146,9 @@ class ClockSampler:
 # ------------------------------------------------------------------ ours -----
 
 class _Dist:
-    def __init__(self, world: int):
+    def __init__(self, world: int, backend: str = "nccl"):
         self.world = world
+        self.device = "cuda" if backend == "nccl" else "cpu"
 
     def max(self, x: float) -> float:
         if self.world == 1:
@@ -155,7 +156,7 @@ class _Dist:
         import torch
         import torch.distributed as dist
 
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=self.device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -305,19 +306,26 @@ def run_ours(args) -> dict | None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
-    torch.cuda.set_device(local)
+    # SQF2K_BENCH_BACKEND=gloo + SQF2K_DEVICE: the N > 1 code path with every
+    # rank on one GPU (tests/test_gpu_multirank.py); the product runs NCCL
+    backend = os.environ.get("SQF2K_BENCH_BACKEND", "nccl")
+    device = int(os.environ.get("SQF2K_DEVICE", local))
+    torch.cuda.set_device(device)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2411_01964_b200 import _lib
 
     _lib.lib()  # bind this rank's GPU; raises without the native library
-    D = _Dist(world)
+    D = _Dist(world, backend)
     stream = torch.cuda.ExternalStream(_lib.stream_handle())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     peak, peak_src = measured_peak_gbs()
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(device)
     head = measure(args.config, args, D, rank, flush, stream, peak, peak_src, clocks)
     secondary = None
     if world == 1 and args.config != "C2" and not args.no_secondary:

@@ -87,3 +87,24 @@ def test_sharded_checkpoint_resume(tmp_path):
     want = _golden_report(1, 1 << 24)
     got = _run(2, dict(start=1, end=1 << 24, segment_width=1 << 20), str(tmp_path / "cp.txt"))
     assert all(r == want for r in got)
+
+
+def test_bench_multirank_path():
+    # bench.py's N > 1 path (torchrun, strong-sharded range, max-over-ranks
+    # timing, NCCL-style all-reduces) with both ranks on cuda:0 under gloo
+    import subprocess
+    import sys
+    env = dict(os.environ, SQF2K_BENCH_BACKEND="gloo", SQF2K_DEVICE="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+         "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+         "--config", "C2", "--steps", "2", "--warmup", "3", "--min-warmup-s", "0"],
+        cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["e2e"]["k_sum"] == 851098084  # the C2 reference k_sum, merged over 2 ranks
+    assert line["value"] > 0 and line["e2e"]["value"] > 0
