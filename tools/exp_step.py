@@ -17,13 +17,14 @@ from paper_2411_01964_b200.runner import verify_range  # noqa: E402
 start = int(eval(args[1])) if len(args) > 1 else (1 << 50) - (1 << 44) + 1
 end = int(eval(args[2])) if len(args) > 2 else 1 << 50
 end += (end - start) % 2
+pipeline = os.environ.get("PIPELINE", "fused")
 for _ in range(3):
-    verify_range(start, end, 30)
+    verify_range(start, end, 30, pipeline=pipeline)
 ts = []
 for _ in range(reps):
     _lib.sync()
     t = time.perf_counter()
-    s = verify_range(start, end, 30)
+    s = verify_range(start, end, 30, pipeline=pipeline)
     ts.append(time.perf_counter() - t)
 name = Path(args[0]).name if args and args[0] != "-" else "main"
 best = min(ts)
