@@ -313,8 +313,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t pari
 #define SQF2K_LPT_PER_TRIP 2.0
 #define SQF2K_LPT_TASK 2.0
 #endif
+#ifndef SQF2K_ITEM_GROWTH
+#define SQF2K_ITEM_GROWTH 1.5
+#endif
 #ifndef SQF2K_SCATTER_UNROLL
-#define SQF2K_SCATTER_UNROLL 4
+#define SQF2K_SCATTER_UNROLL 2
 #endif
 struct MedLane {
     uint32_t o[kTaskSlots], step[kTaskSlots];
@@ -325,6 +328,9 @@ __device__ __forceinline__ void scatter_medium(MedLane &L, uint32_t wbase, uint3
     for (int j = 0; j < kTaskSlots; ++j) {
         const uint32_t st = L.step[j];
         uint32_t o = L.o[j];
+#if SQF2K_SCATTER_UNROLL == 1
+        for (; o < len; o += st) clear_bit(wbase, o);
+#else
 #if SQF2K_SCATTER_UNROLL == 4
         for (; o + 3 * st < len; o += 4 * st) {
             clear_bit(wbase, o);
@@ -341,6 +347,7 @@ __device__ __forceinline__ void scatter_medium(MedLane &L, uint32_t wbase, uint3
             clear_bit(wbase, o);
             o += st;
         }
+#endif
         L.o[j] = st ? o - len : o;  // idle slots (step 0) keep o = ~0
     }
 }
@@ -1094,7 +1101,7 @@ MedTables build_med(const std::vector<uint32_t> &med_primes) {
         double trips;
         uint32_t x, y;
     };
-    for (double item = kItemHits; item <= kTile; item *= 1.5) {
+    for (double item = kItemHits; item <= kTile; item *= SQF2K_ITEM_GROWTH) {
         MedTables t;
         std::vector<Desc> descs;
         for (uint32_t p : med_primes) {

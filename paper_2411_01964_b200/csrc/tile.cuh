@@ -73,7 +73,7 @@ constexpr int kMaxMed = 176;            // pi(1023) - 4 = 168
 #endif
 constexpr int kTaskSlots = SQF2K_TASK_SLOTS;  // 32-lane scatter tasks per warp (registers)
 #ifndef SQF2K_ITEM_HITS
-#define SQF2K_ITEM_HITS 4
+#define SQF2K_ITEM_HITS 7
 #endif
 constexpr int kItemHits = SQF2K_ITEM_HITS;  // target hits per lane per tile (medium schedule)
 #ifndef SQF2K_PATTERN_11
