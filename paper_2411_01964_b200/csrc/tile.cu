@@ -28,6 +28,11 @@ namespace {
 #ifndef SQF2K_START_BARS
 #define SQF2K_START_BARS 1
 #endif
+// the thread that issues the tile starts' bulk copies and waits for them
+#ifndef SQF2K_START_WARP
+#define SQF2K_START_WARP 0
+#endif
+constexpr uint32_t kStarter = 32 * SQF2K_START_WARP;
 // tile starts by one bulk copy from the pattern table need 16-byte aligned
 // sources: four copies of the table, shifted by one word each
 constexpr uint32_t kPatCopies = SQF2K_TMA_START ? 4 : 1;
@@ -505,6 +510,29 @@ __device__ __forceinline__ uint32_t edge_mask(const TileParams &P, uint64_t u0) 
     return pend;
 }
 
+// One word with slots left after the main passes (rare): counted against
+// hist[KMAIN], then deferred to the residue queue (KMAIN = 5) or sent to the
+// escalation / failure list.
+template <int KMAIN>
+__device__ __forceinline__ void leftover_word(TileSmem &S, const TileParams &P, uint32_t hb,
+                                              uint32_t w, uint64_t u0, uint32_t left, uint32_t need,
+                                              uint32_t qi) {
+    if (KMAIN >= 2) atomicAdd(&S.cnt[0], (uint32_t)__popc(left));  // subtracted from hist[KMAIN]
+    if (KMAIN == kMainMax) {
+        const uint32_t e = atomicAdd(&S.n_res[qi], 1u);
+        if (e < (uint32_t)kResCap) {  // deferred to the next tile's scan phase
+            S.res_w[qi][e] = w;
+            S.res_p[qi][e] = left;
+        } else {
+            scan_residue(S, P, hb, w, u0, left, need);
+        }
+    } else if (P.k_max > P.k_eff) {  // k_eff = KMAIN < kMainMax: leftovers leave the tile
+        spill_word(left, u0, P.base_n, P.esc, P.esc_count, P.esc_cap);
+    } else {
+        spill_word(left, u0, P.base_n, P.fail, P.fail_count, P.fail_cap);
+    }
+}
+
 // Exponent passes over the tile (ring buffer at hb): thread t owns the
 // kWordsPerThread consecutive words from W*t, taken 4 at a time (one LDS.128
 // plus the left neighbour).  EDGE masks the scan range, TRACK records per-k
@@ -549,30 +577,9 @@ __device__ __forceinline__ void scan_tile(TileSmem &S, const TileParams &P, uint
         }
         if (!EDGE) scanned += 32 * CW;
         if (any) {  // rare
-            if (KMAIN >= 2) {  // pending after pass KMAIN: subtracted from hist[KMAIN] at the end
-                uint32_t nl = 0;
 #pragma unroll
-                for (int i = 0; i < CW; ++i) nl += __popc(left[i]);
-                atomicAdd(&S.cnt[0], nl);
-            }
-#pragma unroll
-            for (int i = 0; i < CW; ++i) {
-                if (!left[i]) continue;
-                const uint64_t u0 = tb + 32ull * (w0 + i);
-                if (KMAIN == kMainMax) {
-                    const uint32_t e = atomicAdd(&S.n_res[qi], 1u);
-                    if (e < (uint32_t)kResCap) {  // deferred to the next tile's scan phase
-                        S.res_w[qi][e] = w0 + i;
-                        S.res_p[qi][e] = left[i];
-                    } else {
-                        scan_residue(S, P, hb, w0 + i, u0, left[i], need);
-                    }
-                } else if (P.k_max > P.k_eff) {  // k_eff = KMAIN < kMainMax: leftovers leave the tile
-                    spill_word(left[i], u0, P.base_n, P.esc, P.esc_count, P.esc_cap);
-                } else {
-                    spill_word(left[i], u0, P.base_n, P.fail, P.fail_count, P.fail_cap);
-                }
-            }
+            for (int i = 0; i < CW; ++i)
+                if (left[i]) leftover_word<KMAIN>(S, P, hb, w0 + i, tb + 32ull * (w0 + i), left[i], need, qi);
         }
     }
 #pragma unroll
@@ -758,18 +765,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         auto start_tile = [&](uint32_t t, uint32_t at) {  // tile t's words (ring base at)
             const uint64_t tb = (uint64_t)t * kTile;
 #ifdef SQF2K_CHECKS
-            if (threadIdx.x == 0) S.tag[t % kRingTiles] = t;
+            if (threadIdx.x == kStarter) S.tag[t % kRingTiles] = t;
 #endif
             if (t < ti0 || t >= ti1) {
                 init_words<kTileWords, true>(S.ring, at, tb, pbase, P);
-                if (kStartBars && threadIdx.x == 0)  // keep the buffer's phase count
+                if (kStartBars && threadIdx.x == kStarter)  // keep the buffer's phase count
                     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
                                      smem_addr(&S.start_bar[t % kRingTiles]))
                                  : "memory");
             } else if (kTmaStart) {
                 // one bulk copy (TMA) of the pattern words, from the shifted
                 // table copy that makes the source 16-byte aligned
-                if (threadIdx.x == 0) {
+                if (threadIdx.x == kStarter) {
                     const uint32_t r = pbase & 3u;
                     const uint32_t bar = smem_addr(kStartBars ? &S.start_bar[t % kRingTiles] : &S.mbar_start);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -792,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         };
         // thread 0, before the barrier that publishes a start: its copy has landed
         auto finish_start = [&]() {
-            if (kTmaStart && threadIdx.x == 0 && start_pending) {
+            if (kTmaStart && threadIdx.x == kStarter && start_pending) {
                 uint32_t done = 0;
                 while (!done)
                     asm volatile(
@@ -816,7 +823,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             uint32_t bytes = 0;
             for (uint32_t i = 0; i < n; ++i)
                 if (!edge_t(ta + i)) bytes += (uint32_t)kTileWords * 4;
-            if (kTmaStart && bytes && threadIdx.x == 0) {
+            if (kTmaStart && bytes && threadIdx.x == kStarter) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                                  smem_addr(&S.mbar_start)),
@@ -828,12 +835,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                 const uint32_t t = ta + i, at = ring_base(t);
                 const uint64_t tb = (uint64_t)t * kTile;
 #ifdef SQF2K_CHECKS
-                if (threadIdx.x == 0) S.tag[t % kRingTiles] = t;
+                if (threadIdx.x == kStarter) S.tag[t % kRingTiles] = t;
 #endif
                 if (edge_t(t)) {
                     init_words<kTileWords, true>(S.ring, at, tb, pbase, P);
                 } else if (kTmaStart) {
-                    if (threadIdx.x == 0) {
+                    if (threadIdx.x == kStarter) {
                         const uint32_t r = pbase & 3u;
                         asm volatile(
                             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
