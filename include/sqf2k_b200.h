@@ -82,7 +82,7 @@ typedef struct sqf2k_verify_opts {
                               the tile depth but k_max > depth escalates to the
                               exact trial-division kernel.  Tests force tiny
                               depths to exercise escalation.                   */
-    uint64_t batch_slots;  /* odd slots per device batch; 0 = default 2^36, max 2^40 */
+    uint64_t batch_slots;  /* odd slots per device batch; 0 = default 2^37, max 2^40 */
     uint32_t flags;        /* SQF2K_EXACT_BUCKETS: exact (count + scan) large-
                               prime lists from the start instead of the fixed-
                               capacity lists with exact fallback (tests)      */

@@ -318,6 +318,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t pari
 #define SQF2K_LPT_PER_TRIP 2.0
 #define SQF2K_LPT_TASK 2.0
 #endif
+#ifndef SQF2K_LPT_WARP_BIAS
+#define SQF2K_LPT_WARP_BIAS 0.5
+#endif
 #ifndef SQF2K_ITEM_GROWTH
 #define SQF2K_ITEM_GROWTH 1.5
 #endif
@@ -1133,6 +1136,8 @@ MedTables build_med(const std::vector<uint32_t> &med_primes) {
         if (n_tasks > (uint32_t)(kWarps * kTaskSlots)) continue;
         std::vector<double> load(kWarps, 0.0);
         load[kWarps - 1] = SQF2K_LPT_BUCKET;  // the bucket warp (scatter_bucket)
+        // the warp schedulers favour high warp ids: pre-charge the low ones
+        for (int w = 0; w < kWarps; ++w) load[w] += SQF2K_LPT_WARP_BIAS * (kWarps - 1 - w);
         std::vector<int> used(kWarps, 0);
         t.tasks.assign((size_t)kWarps * kTaskSlots * 64, 0u);  // step 0: idle lane
         for (uint32_t k = 0; k < n_tasks; ++k) {  // longest first, least-loaded warp with room

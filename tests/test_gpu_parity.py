@@ -434,3 +434,24 @@ def test_window_shards_match_reference(log2w):
         assert got.k_sum == want["k_sum"]
         assert {str(m): n for m, n in got.record_candidates.items()} == want["record_candidates"]
         assert got.failures == want["failures"]
+
+
+def test_smallest_exponent_matches_scan_exponents():
+    # search.py:66-90 scalar lookup against the GPU per-slot exponents and the
+    # reference's known answers (test_search.py:25-31): 3, 5, 11, 29, 533, 849
+    from paper_2411_01964_b200.search import smallest_exponent
+    p = generate_primes(1 << 12)
+    cur = sieve_segment(1, 1 << 12 | 1, p)
+    w = SegmentWindow(None, cur)
+    for n, k in [(3, 1), (5, 1), (11, 2), (29, 3), (533, 4), (849, 5), (127, 2)]:
+        out = smallest_exponent(n, w, 12)
+        assert out.found and out.k == k, (n, out)
+    kv = scan_exponents(w, 12)
+    rng = random.Random(11)
+    for n in rng.sample(range(3, 1 << 12, 2), 200):
+        out = smallest_exponent(n, w, 12)
+        assert (out.k if out.found else 0) == int(kv[(n - 1) // 2]), n
+    with pytest.raises(ValueError):
+        smallest_exponent(4, w, 12)
+    with pytest.raises(ValueError):
+        smallest_exponent(11, w, 0)

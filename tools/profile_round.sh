@@ -3,8 +3,8 @@
 #   bash tools/profile_round.sh TAG
 # bench lines (C5 headline + C2 secondary + CPU baseline, the reference arm,
 # C3 and C4), the paper's [1, 2^50) with clocks, the ncu launch list of the
-# bench command, and one `ncu --set full` capture each of tile_fused (2^36
-# window ending at 2^50, C5's regime) and window_scan (2^37 window).
+# bench command, and one `ncu --set full` capture each of tile_fused (one C5
+# batch: the 2^38-integer window ending at 2^50) and window_scan (2^37 window).
 # Outputs land in gpurun_out/; tools/summarize_round.py turns them into
 # profiles/ files.
 TAG=${1:-r2}
@@ -21,9 +21,10 @@ python $B > $O/${TAG}_launch_plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv \
       --log-file $O/${TAG}_launches_c5.csv python $B > $O/${TAG}_launch_ncu.log 2>&1; echo launches=$?
 # full captures: the fused tile kernel near 2^50, the window scan
-python tools/exp_time.py - > $O/${TAG}_plain_tile.log 2>&1 && \
+W="(1<<50)-(1<<38)+1"  # 2^37 odd slots: exactly one C5 batch
+python tools/exp_time.py - "$W" "1<<50" > $O/${TAG}_plain_tile.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:tile_kernel -s 2 -c 1 \
-      -o $O/${TAG}_prof_tile_c5 python tools/exp_time.py - > $O/${TAG}_ncu_tile.log 2>&1; echo ncu_tile=$?
+      -o $O/${TAG}_prof_tile_c5 python tools/exp_time.py - "$W" "1<<50" > $O/${TAG}_ncu_tile.log 2>&1; echo ncu_tile=$?
 PIPELINE=bitmap python tools/exp_time.py - "(1<<50)-(1<<37)+1" "1<<50" > $O/${TAG}_plain_scan.log 2>&1 && \
   PIPELINE=bitmap ncu --set full --clock-control none --import-source on -k regex:wscan -s 2 -c 1 \
       -o $O/${TAG}_prof_wscan python tools/exp_time.py - "(1<<50)-(1<<37)+1" "1<<50" > $O/${TAG}_ncu_scan.log 2>&1; echo ncu_scan=$?

@@ -51,9 +51,9 @@ if lst.exists():
 
 traffic_path = P / "ncu_traffic.json"
 traffic = json.loads(traffic_path.read_text()) if traffic_path.exists() else {}
-# (the tile capture is a 2^35-slot launch, half of a C5 batch: bytes scaled x2
-# to C5's 2^36-slot launch; the scan capture is the 2^37 window's 2^36 slots)
-for rep, out, key, algo, scale in [(f"{tag}_prof_tile_c5", f"{tag}_ncu_tile_fused_c5.txt", "tile_fused@C5", 2 ** 36 * 0.25, 2.0),
+# (the tile capture is one 2^37-slot C5 batch; the scan capture is the 2^37
+# window's 2^36 slots)
+for rep, out, key, algo, scale in [(f"{tag}_prof_tile_c5", f"{tag}_ncu_tile_fused_c5.txt", "tile_fused@C5", 2 ** 37 * 0.25, 1.0),
                                    (f"{tag}_prof_wscan", f"{tag}_ncu_window_scan.txt", "window_scan@2p37", 2 ** 36 / 8, 1.0)]:
     r = O / f"{rep}.ncu-rep"
     if not r.exists():
@@ -73,6 +73,6 @@ for rep, out, key, algo, scale in [(f"{tag}_prof_tile_c5", f"{tag}_ncu_tile_fuse
                     "dram_bytes_per_launch": scale * (b("dram__bytes_read.sum") + b("dram__bytes_write.sum")),
                     "algorithmic_bytes_per_launch": algo,
                     "source": f"profiles/{out} (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum"
-                              + (", x2 from a 2^35-slot launch)" if scale != 1.0 else ")")}
+                              + (f", x{scale:g} from a smaller launch)" if scale != 1.0 else ")")}
 traffic_path.write_text(json.dumps(traffic, indent=1) + "\n")
 print("profiles written")
