@@ -92,6 +92,13 @@ __device__ __forceinline__ uint64_t mod_q(uint64_t a, uint64_t q, double inv_q) 
     return (uint64_t)r;
 }
 
+// slot_residue (tile.cuh) through mod_q: the first slot u >= 0 with q | base_n + 2u
+__device__ __forceinline__ uint64_t slot_residue_q(int64_t base_n, uint64_t q, double inv_q) {
+    const uint64_t a = base_n >= 0 ? mod_q((uint64_t)base_n, q, inv_q) : 0u;
+    const uint64_t an = base_n >= 0 ? (a ? q - a : 0) : mod_q((uint64_t)(-base_n), q, inv_q);
+    return (an & 1) ? (an + q) / 2 : an / 2;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) bucket_kernel(
     const uint32_t *__restrict__ primes, const PrimeInfo *__restrict__ info, int64_t base_n,
@@ -146,9 +153,7 @@ __global__ void __launch_bounds__(256) bucket_kernel(
         const uint64_t q = p * p;
         const double inv_q = 1.0 / (double)q;
         // first slot u >= 0 with q | base_n + 2u (slot_residue), by mod_q
-        const uint64_t a = base_n >= 0 ? mod_q((uint64_t)base_n, q, inv_q) : 0u;
-        const uint64_t an = base_n >= 0 ? (a ? q - a : 0) : mod_q((uint64_t)(-base_n), q, inv_q);
-        const uint64_t r = (an & 1) ? (an + q) / 2 : an / 2;
+        const uint64_t r = slot_residue_q(base_n, q, inv_q);
         const uint64_t lm = mod_q(lo, q, inv_q);
         // <= 5 hits (q >= 2^(20+2j), range 2^(22+2j)): all atomics in flight
         // together, then the stores -- one round trip, not one per hit
@@ -370,8 +375,9 @@ __device__ __forceinline__ void init_medium(MedLane &L, const TileParams &P, uin
         L.o[j] = ~0u;
         if (d.y) {
             const uint32_t q = __ldg(&P.med[d.x & 0xffu]);
-            const uint32_t r = (uint32_t)slot_residue(P.base_n, q);
-            const uint32_t bm = (uint32_t)(b0 % q);
+            const double inv_q = 1.0 / (double)q;
+            const uint32_t r = (uint32_t)slot_residue_q(P.base_n, q, inv_q);
+            const uint32_t bm = (uint32_t)mod_q(b0, q, inv_q);
             L.o[j] = (r >= bm ? r - bm : r + q - bm) + (d.x >> 8) * q;
         }
     }
@@ -760,7 +766,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         // medium primes: each lane's descriptors, first hits at the chunk base b0
         const uint64_t b0 = pre ? (uint64_t)t0 * kTile - H : (uint64_t)t0 * kTile;
         MedLane L;
-        init_medium(L, P, b0);
         if (threadIdx.x < 2) S.n_res[threadIdx.x] = 0;
         // pattern index of the next tile start (t0 first; the halo has its own)
         uint32_t pbase = (uint32_t)(((uint64_t)t0 * kTileWords) % kPatWords);
@@ -862,6 +867,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
 #if SQF2K_SPLIT_PHASE
         start_batch(t0, min(3u, t1 - t0));  // in flight during the halo work below
 #endif
+        init_medium(L, P, b0);  // (after the starts: its table loads overlap their copies)
 
         // the halo just below tile t0: the tail of buffer t0 - 1
         const uint32_t halo_at = ring_base(t0 + kRingTiles - 1) + kTileWords - HW;
