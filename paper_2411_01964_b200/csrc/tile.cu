@@ -36,35 +36,44 @@ constexpr uint32_t kStarter = 32 * SQF2K_START_WARP;
 // tile starts by one bulk copy from the pattern table need 16-byte aligned
 // sources: four copies of the table, shifted by one word each
 constexpr uint32_t kPatCopies = SQF2K_TMA_START ? 4 : 1;
-constexpr uint32_t kPatStride = (kPatWords + kTileWords + 3) / 4 * 4;
+constexpr uint32_t kPatStride = (kPatWordsMax + kTileWords + 3) / 4 * 4;
 
 // -------------------------------------------------------------------------
 // p = 3, 5, 7 (11): word g of the domain (slots 32g..32g+31) with every slot
-// u such that 9, 25, 49 (or 121) divides n(u) cleared.  Period kPatWords
+// u such that 9, 25, 49 (or 121) divides n(u) cleared.  Period pattern_words
 // words; the first kTileWords words are repeated after the period so that a
 // tile's words [pbase, pbase + kTileWords) never wrap.
 // First hit at or after 32g: y = (r - 32g) mod q; the word's hits are the
 // bits y, y+q, ... < 32, i.e. (bits 0, q, 2q, ...) << y.
 __global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__restrict__ table) {
-    constexpr int NP = kPattern11 ? 4 : 3;
+    const int NP = (present & 8u) ? 4 : 3;
     const uint32_t q[4] = {9, 25, 49, 121};
     const uint32_t pat[4] = {0x08040201u, 0x02000001u, 0x1u, 0x1u};
-    uint32_t r[4];
+    // Thread i computes words g = i, i + T, ... (T threads: a warp's stores
+    // are coalesced) and steps each first-hit offset by -32T slots mod q
+    // instead of dividing per word.  Word g is computed once and stored into
+    // every shifted copy: copy r (at table + r * kPatStride) holds word g at
+    // index g - r, so a tile start at any pattern index has a 16-byte
+    // aligned source.
+    const uint32_t T = gridDim.x * blockDim.x, g0 = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t y[4], dec[4];
 #pragma unroll
-    for (int i = 0; i < NP; ++i) r[i] = (uint32_t)slot_residue(base_n, q[i]);
-    // copy r (r = 0..kPatCopies-1) at table + r * kPatStride holds word g + r at
-    // index g, so a tile start at any pattern index has a 16-byte aligned source
-    for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < kPatCopies * kPatStride;
-         gi += gridDim.x * blockDim.x) {
-        const uint32_t g = gi % kPatStride + gi / kPatStride;
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t r = (uint32_t)slot_residue(base_n, q[i]);
+        y[i] = (r + q[i] - (uint32_t)((32ull * g0) % q[i])) % q[i];
+        dec[i] = (uint32_t)((32ull * T) % q[i]);
+    }
+    const uint32_t words = min(pattern_words(present) + kTileWords, kPatStride) + kPatCopies - 1;
+    for (uint32_t g = g0; g < words; g += T) {
         uint32_t clr = 0;
 #pragma unroll
-        for (int i = 0; i < NP; ++i) {
-            if (!((present >> i) & 1u)) continue;
-            const uint32_t y = (r[i] + q[i] - (32u * g) % q[i]) % q[i];
-            if (y < 32) clr |= pat[i] << y;
+        for (int i = 0; i < 4; ++i) {
+            if (i < NP && ((present >> i) & 1u) && y[i] < 32) clr |= pat[i] << y[i];
+            y[i] = y[i] >= dec[i] ? y[i] - dec[i] : y[i] + q[i] - dec[i];
         }
-        table[gi] = ~clr;
+#pragma unroll
+        for (uint32_t r = 0; r < kPatCopies; ++r)
+            if (g >= r && g - r < kPatStride) table[r * kPatStride + (g - r)] = ~clr;
     }
 }
 
@@ -276,9 +285,18 @@ constexpr uint32_t kWaitSleepNs = SQF2K_WAIT_SLEEP_NS;
 #ifndef SQF2K_NAMED_BAR
 #define SQF2K_NAMED_BAR 0
 #endif
+// SQF2K_WARP_ARRIVE: one arrival per warp (lane 0 after __syncwarp) instead
+// of one per thread
+#ifndef SQF2K_WARP_ARRIVE
+#define SQF2K_WARP_ARRIVE 0
+#endif
+constexpr uint32_t kPhaseArrivals = SQF2K_WARP_ARRIVE ? kThreads / 32 : kThreads;
 __device__ __forceinline__ void phase_arrive(unsigned long long *bar, uint32_t phase) {
 #if SQF2K_NAMED_BAR
     asm volatile("bar.arrive %0, %1;" ::"r"(1u + (phase & 1u)), "r"(2u * kThreads) : "memory");
+#elif SQF2K_WARP_ARRIVE
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
 #else
     mbar_arrive(bar);
 #endif
@@ -410,7 +428,7 @@ __device__ __forceinline__ void scatter_bucket(uint32_t wbase, const TileParams 
 
 // Start WORDS words (domain slot `base`, ring word `at`, 16-byte aligned and
 // not wrapping) from the p = 3, 5, 7 pattern; pbase is (base / 32) mod
-// kPatWords.  Thread i writes the 4-word chunks i, i + kThreads, ... with
+// pat_words.  Thread i writes the 4-word chunks i, i + kThreads, ... with
 // one STS.128 each.  EDGE applies the n < 1 zero region and the domain end.
 template <int WORDS, bool EDGE>
 __device__ __forceinline__ void init_words(uint32_t *ring, uint32_t at, uint64_t base,
@@ -673,7 +691,7 @@ __device__ __forceinline__ void tl_tile(uint32_t i) {
 #define TLT(i) do { } while (0)
 #endif
 
-template <bool FUSED, int KMAIN>
+template <bool FUSED, int KMAIN, bool PAT11>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TileParams P) {
     static_assert(kWordsPerThread % 4 == 0 && kThreads * kWordsPerThread == kTileWords,
                   "4-word chunks per thread");
@@ -744,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     if (threadIdx.x < kThreads / 32) S.wphase[threadIdx.x] = 0;
     if (threadIdx.x < kRingTiles) S.tag[threadIdx.x] = ~0u;
 #endif
-    if (threadIdx.x == 0) mbar_init(&S.mbar, kThreads);
+    if (threadIdx.x == 0) mbar_init(&S.mbar, kPhaseArrivals);
     __syncthreads();
 #endif
 
@@ -768,8 +786,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         MedLane L;
         if (threadIdx.x < 2) S.n_res[threadIdx.x] = 0;
         // pattern index of the next tile start (t0 first; the halo has its own)
-        uint32_t pbase = (uint32_t)(((uint64_t)t0 * kTileWords) % kPatWords);
-        const uint32_t pbase_halo = (uint32_t)((b0 / 32) % kPatWords);
+        // the period as a compile-time constant (a runtime P.pat_words
+        // measured 0.5 % slower on the C5 window)
+        constexpr uint32_t pat_words = pattern_words(PAT11 ? 8u : 0u);
+        uint32_t pbase = (uint32_t)(((uint64_t)t0 * kTileWords) % pat_words);
+        const uint32_t pbase_halo = (uint32_t)((b0 / 32) % pat_words);
         auto start_tile = [&](uint32_t t, uint32_t at) {  // tile t's words (ring base at)
             const uint64_t tb = (uint64_t)t * kTile;
 #ifdef SQF2K_CHECKS
@@ -803,7 +824,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                 init_words<kTileWords, false>(S.ring, at, tb, pbase, P);
             }
             pbase += kTileWords;
-            if (pbase >= kPatWords) pbase -= kPatWords;
+            if (pbase >= pat_words) pbase -= pat_words;
         };
         // thread 0, before the barrier that publishes a start: its copy has landed
         auto finish_start = [&]() {
@@ -861,7 +882,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                     init_words<kTileWords, false>(S.ring, at, tb, pbase, P);
                 }
                 pbase += kTileWords;
-                if (pbase >= kPatWords) pbase -= kPatWords;
+                if (pbase >= pat_words) pbase -= pat_words;
             }
         };
 #if SQF2K_SPLIT_PHASE
@@ -1171,7 +1192,11 @@ struct MedCache {
     DevBuf buf;  // kMaxMed q values, then the task table
 };
 
-MedCache g_med;  // the library serialises calls
+// one schedule per pattern kind (11 in the table or in the scatter), so
+// calls alternating between small and large domains rebuild nothing; the
+// library serialises calls
+MedCache g_med[2];
+MedCache &med_cache(const BatchArgs &a) { return g_med[(a.pattern_present >> 3) & 1u]; }
 
 }  // namespace
 
@@ -1193,20 +1218,28 @@ size_t tile_smem_bytes() { return sizeof(TileSmem); }
 // of (U/p^2 + 1) <= U / (2 * 1029) + n_bucket_primes.
 uint64_t bucket_hits_bound(uint64_t U, uint64_t n_bucket) { return U / 2058 + 1 + n_bucket; }
 
-template <bool FUSED, int KMAIN>
-void launch_tile(const char *name, unsigned grid, size_t smem, const TileParams &P) {
+template <bool FUSED, int KMAIN, bool PAT11>
+void launch_tile_as(const char *name, unsigned grid, size_t smem, const TileParams &P) {
     static bool attr = false;
     if (!attr) {
-        SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<FUSED, KMAIN>,
+        SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<FUSED, KMAIN, PAT11>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         // carve only the shared memory kCtasPerSm CTAs need: the rest stays L1,
         // which holds the pattern table every tile reads
         const int pct = (int)((kCtasPerSm * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
-        SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<FUSED, KMAIN>,
+        SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<FUSED, KMAIN, PAT11>,
                                         cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         attr = true;
     }
-    launch_pdl(name, tile_kernel<FUSED, KMAIN>, dim3(grid), dim3(kThreads), smem, P);
+    launch_pdl(name, tile_kernel<FUSED, KMAIN, PAT11>, dim3(grid), dim3(kThreads), smem, P);
+}
+
+template <bool FUSED, int KMAIN>
+void launch_tile(const char *name, unsigned grid, size_t smem, const TileParams &P) {
+    if (kPattern11 && P.pat_words == pattern_words(8u))
+        launch_tile_as<FUSED, KMAIN, kPattern11>(name, grid, smem, P);
+    else
+        launch_tile_as<FUSED, KMAIN, false>(name, grid, smem, P);
 }
 
 // Work of a batch that does not need the prime table: the medium schedule
@@ -1217,14 +1250,15 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
 
     // medium tables: cached per distinct prime set
     constexpr size_t kTaskWords = (size_t)(kThreads / 32) * kTaskSlots * 64;
-    if (g_med.key != *a.med_primes || !g_med.buf.ptr) {
+    MedCache &med = med_cache(a);
+    if (med.key != *a.med_primes || !med.buf.ptr) {
         MedTables t = build_med(*a.med_primes);
-        g_med.key = *a.med_primes;
-        g_med.buf.reserve((kMaxMed + kTaskWords) * 4);
+        med.key = *a.med_primes;
+        med.buf.reserve((kMaxMed + kTaskWords) * 4);
         std::vector<uint32_t> host(kMaxMed + kTaskWords, 0);
         std::copy(t.q.begin(), t.q.end(), host.begin());
         std::copy(t.tasks.begin(), t.tasks.end(), host.begin() + kMaxMed);
-        SQF2K_CUDA(cudaMemcpy(g_med.buf.ptr, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
+        SQF2K_CUDA(cudaMemcpy(med.buf.ptr, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
         dev_alloc_bump();  // captured graphs read this table
     }
 
@@ -1233,7 +1267,9 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
     DevBuf &counts = a.buf ? c.tile_counts_b : c.tile_counts;
     pattern.reserve((size_t)kPatCopies * kPatStride * 4);
     launch_on(st, "pattern", pattern_kernel,
-              dim3((unsigned)std::min<uint64_t>(ceil_div(kPatCopies * kPatStride, 256), c.sm_count * 8)), dim3(256),
+              dim3((unsigned)std::min<uint64_t>(ceil_div(pattern_words(a.pattern_present) + kTileWords, 256),
+                                                c.sm_count * 8)),
+              dim3(256),
               0, a.base_n, a.pattern_present, pattern.as<uint32_t>());
     const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);
     counts.reserve((n_bt + 1) * 4);
@@ -1315,9 +1351,10 @@ void run_tile_batch(const BatchArgs &a) {
     P.k_eff = a.k_eff;
     P.k_max = a.k_max;
 
+    P.pat_words = pattern_words(a.pattern_present);
     P.pattern = (a.buf ? c.pattern_b : c.pattern).as<uint32_t>();
-    P.med = g_med.buf.as<uint32_t>();
-    P.tasks = reinterpret_cast<const uint2 *>(g_med.buf.as<uint32_t>() + kMaxMed);
+    P.med = med_cache(a).buf.as<uint32_t>();
+    P.tasks = reinterpret_cast<const uint2 *>(med_cache(a).buf.as<uint32_t>() + kMaxMed);
     P.tile_start = tile_start;
     P.tile_count = counts;
     P.hits = hits.as<uint16_t>();

@@ -73,17 +73,27 @@ constexpr int kMaxMed = 176;            // pi(1023) - 4 = 168
 #endif
 constexpr int kTaskSlots = SQF2K_TASK_SLOTS;  // 32-lane scatter tasks per warp (registers)
 #ifndef SQF2K_ITEM_HITS
-#define SQF2K_ITEM_HITS 7
+#define SQF2K_ITEM_HITS 5
 #endif
 constexpr int kItemHits = SQF2K_ITEM_HITS;  // target hits per lane per tile (medium schedule)
 #ifndef SQF2K_PATTERN_11
-#define SQF2K_PATTERN_11 0
+#define SQF2K_PATTERN_11 1
 #endif
-// p = 3, 5, 7 (and optionally 11: measured no faster) are applied as one
-// periodic word pattern: period
-// 9*25*49 words (*121 with 11: 1.33 M words, 5.3 MB, L2-resident)
+// p = 3, 5, 7 (and 11) are applied as one periodic word pattern: period
+// 9*25*49 words, or 9*25*49*121 with 11 (1.33 M words, 5.3 MB per copy,
+// L2-resident).  Taking 11 (541 hits per 2^16-slot tile, 27 % of the medium
+// scatter) out of the scatter measured 484.6 -> 467.7 ms per C5 call together
+// with ~5-hit descriptors; building the larger table costs ~4 us per batch,
+// so domains below kPattern11MinSlots keep 11 in the scatter (C2: 0.088 vs
+// 0.092 ms per call).  SQF2K_PATTERN_11=0 never uses it.
 constexpr bool kPattern11 = SQF2K_PATTERN_11 != 0;
-constexpr uint32_t kPatWords = 9 * 25 * 49 * (kPattern11 ? 121 : 1);
+constexpr uint32_t kPatWords3 = 9 * 25 * 49;
+constexpr uint32_t kPatWordsMax = kPatWords3 * (kPattern11 ? 121 : 1);
+constexpr uint64_t kPattern11MinSlots = 1ull << 30;
+// period of the table whose present mask is `present` (bit 3: prime 11)
+__host__ __device__ constexpr uint32_t pattern_words(uint32_t present) {
+    return (present & 8u) ? kPatWords3 * 121 : kPatWords3;
+}
 #ifndef SQF2K_MIN_CHUNK
 #define SQF2K_MIN_CHUNK 4
 #endif
@@ -134,7 +144,8 @@ struct TileParams {
     uint32_t n_btiles;   // bucket tiles (2^16 slots) in the domain
     uint32_t k_eff;      // passes inside the tile
     uint32_t k_max;      // run limit: escalate when k_max > k_eff
-    const uint32_t *pattern;     // p = 3, 5, 7 (11) mask by u-word mod kPatWords (+ kTileWords
+    uint32_t pat_words;          // period of the pattern table (pattern_words)
+    const uint32_t *pattern;     // p = 3, 5, 7 (11) mask by u-word mod pat_words (+ kTileWords
                                  // repeated words, so a tile never wraps)
     const uint32_t *med;         // q = p^2 of the medium primes
     const uint2 *tasks;          // [warp][kTaskSlots][lane]: (m | mult << 8, step), step 0 idle

@@ -99,7 +99,7 @@ struct SmallSet {
     uint32_t present = 0;
 };
 
-SmallSet small_set_upto_impl(uint64_t limit) {
+SmallSet small_set_upto_impl(uint64_t limit, bool with11) {
     static const std::vector<uint32_t> all = small_primes(kPMed);
     SmallSet s;
     for (uint32_t p : all) {
@@ -107,18 +107,21 @@ SmallSet small_set_upto_impl(uint64_t limit) {
         if (p == 3) s.present |= 1;
         else if (p == 5) s.present |= 2;
         else if (p == 7) s.present |= 4;
-        else if (p == 11 && kPattern11) s.present |= 8;
+        else if (p == 11 && with11) s.present |= 8;
         else if (p >= 11) s.med.push_back(p);
     }
     return s;
 }
 
-SmallSet small_set_upto(uint64_t limit) {
+// 11 joins the pattern table for domains of kPattern11MinSlots slots or more
+SmallSet small_set_upto(uint64_t limit, uint64_t n_slots) {
+    const bool with11 = kPattern11 && n_slots >= kPattern11MinSlots;
     if (limit >= kPMed) {  // every range above 2^20: the full set, built once
-        static const SmallSet full = small_set_upto_impl(kPMed);
-        return full;
+        static const SmallSet full[2] = {small_set_upto_impl(kPMed, false),
+                                         small_set_upto_impl(kPMed, true)};
+        return full[with11];
     }
-    return small_set_upto_impl(limit);
+    return small_set_upto_impl(limit, with11);
 }
 
 }  // namespace
@@ -395,7 +398,7 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
     pl.n_slots = (end - start) / 2;
     pl.limit = isqrt_u64(end - 1);
     pl.pipeline = o.pipeline;
-    pl.small = small_set_upto(pl.limit);
+    pl.small = small_set_upto(pl.limit, pl.n_slots);
     pl.esc_cap = 1 << 16;
     pl.dev_fail_cap = std::max<uint64_t>(fail_cap, 1 << 12);
     pl.exact = (o.flags & SQF2K_EXACT_BUCKETS) != 0;
@@ -499,7 +502,7 @@ int sieve_bits(uint64_t start, uint64_t end, const int64_t *primes_h, uint64_t n
         if (p == 3) small.present |= 1;
         else if (p == 5) small.present |= 2;
         else if (p == 7) small.present |= 4;
-        else if (p == 11 && kPattern11) small.present |= 8;
+        else if (p == 11 && kPattern11 && n_slots >= kPattern11MinSlots) small.present |= 8;
         else if (p >= 11) small.med.push_back(p);
     }
     const uint32_t nt = (uint32_t)ceil_div(n_slots, kTile);
