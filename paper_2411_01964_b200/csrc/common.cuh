@@ -67,6 +67,10 @@ struct Context {
     // side stream for work independent of the prime table (fork/join by events,
     // captured into the same graph as parallel branches)
     cudaStream_t side = nullptr;
+    // launch priorities (SQF2K_PRIORITY=1): main-stream kernels outrank the
+    // side stream's, so a ready tile kernel takes the SMs ahead of the next
+    // batch's bucket fill (measured no different on C4: off by default)
+    int prio_main = 0, prio_side = 0;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // multi-batch calls: batch b's bucket lists are built on the side stream
     // (buffer set b & 1) while batch b - 1's tile kernel runs
@@ -102,53 +106,60 @@ struct Context {
 Context &ctx();            // throws Error{SQF2K_ENODEV} if not initialised
 Context *ctx_or_null();
 
-// Launch `kernel` on stream `st`, bracketed by events when profiling.
-template <class Kernel, class... Args>
-void launch_on(cudaStream_t st, const char *name, Kernel kernel, dim3 grid, dim3 block,
-               size_t smem, Args... args) {
+#ifndef SQF2K_PRIORITY
+#define SQF2K_PRIORITY 0
+#endif
+
+// Launch `kernel` on stream `st` (`pdl`: programmatic dependent launch -- the
+// kernel may start while its stream predecessor is still running, once that
+// grid triggers, and must execute griddepcontrol.wait before touching the
+// predecessor's output), with the stream's priority as a launch attribute
+// (kept by graph capture), bracketed by events when profiling.
+template <class... KArgs, class... Args>
+void launch_ex(cudaStream_t st, bool pdl, const char *name, void (*kernel)(KArgs...), dim3 grid,
+               dim3 block, size_t smem, Args... args) {
     Context &c = ctx();
     cudaEvent_t a = nullptr, b = nullptr;
-    if (c.profiling) {
+    if (c.profiling) {  // per-launch events would serialise PDL anyway
         a = c.get_event();
         b = c.get_event();
         SQF2K_CUDA(cudaEventRecord(a, st));
     }
-    kernel<<<grid, block, smem, st>>>(args...);
-    SQF2K_CUDA(cudaGetLastError());
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    static const bool no_pdl = std::getenv("SQF2K_NO_PDL") != nullptr;  // A/B experiments
+    if (pdl && !no_pdl) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n++].val.programmaticStreamSerializationAllowed = c.profiling ? 0 : 1;
+    }
+    if (SQF2K_PRIORITY) {
+        attr[n].id = cudaLaunchAttributePriority;
+        attr[n++].val.priority = st == c.side ? c.prio_side : c.prio_main;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    SQF2K_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
     if (c.profiling) {
         SQF2K_CUDA(cudaEventRecord(b, st));
         c.pending.push_back({c.stat_index(name), a, b});
     }
 }
 
-// Launch with programmatic dependent launch: the kernel may start while its
-// stream predecessor is still running (once that grid triggers) and must
-// execute griddepcontrol.wait before touching the predecessor's output.
+template <class... KArgs, class... Args>
+void launch_on(cudaStream_t st, const char *name, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+               size_t smem, Args... args) {
+    launch_ex(st, false, name, kernel, grid, block, smem, args...);
+}
+
 template <class... KArgs, class... Args>
 void launch_pdl(const char *name, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                 Args... args) {
-    Context &c = ctx();
-    cudaEvent_t a = nullptr, b = nullptr;
-    if (c.profiling) {  // per-launch events would serialise anyway
-        a = c.get_event();
-        b = c.get_event();
-        SQF2K_CUDA(cudaEventRecord(a, c.stream));
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = c.stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = c.profiling ? 0 : 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    SQF2K_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
-    if (c.profiling) {
-        SQF2K_CUDA(cudaEventRecord(b, c.stream));
-        c.pending.push_back({c.stat_index(name), a, b});
-    }
+    launch_ex(ctx().stream, true, name, kernel, grid, block, smem, args...);
 }
 
 // griddepcontrol (sm_90+): wait for the predecessor grid / let the dependent start

@@ -146,11 +146,15 @@ int sqf2k_init(int device) {
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
     c->smem_optin = prop.sharedMemPerBlockOptin;
-    if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+    cudaDeviceGetStreamPriorityRange(&c->prio_side, &c->prio_main);  // (least, greatest)
+    if (!SQF2K_PRIORITY) c->prio_side = c->prio_main = 0;
+    if ((e = cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, c->prio_main)) !=
+        cudaSuccess) {
         delete c;
         return fail(SQF2K_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
     }
-    if ((e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking)) != cudaSuccess ||
+    if ((e = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, c->prio_side)) !=
+            cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_primes, cudaEventDisableTiming)) != cudaSuccess ||

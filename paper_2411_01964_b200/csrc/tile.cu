@@ -342,7 +342,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t pari
 #define SQF2K_LPT_TASK 2.0
 #endif
 #ifndef SQF2K_LPT_WARP_BIAS
-#define SQF2K_LPT_WARP_BIAS 0.5
+#define SQF2K_LPT_WARP_BIAS 0.25
 #endif
 #ifndef SQF2K_ITEM_GROWTH
 #define SQF2K_ITEM_GROWTH 1.5
@@ -940,8 +940,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             // tiles come in increasing order and residue words finish in
             // tile order); stop tracking a k once it is known (warp 0 folds
             // tile t - 1's scan minima into S.first and clears S.need bits
-            // in this phase: a stale read only tracks once more).
-            const uint32_t need = S.need;
+            // in this phase: a stale read only tracks once more).  The value
+            // must be warp-uniform -- it selects the TRACK path, whose warp
+            // reductions need all 32 lanes -- so lane 0's read is broadcast:
+            // lanes of a diverged warp reading S.need before and after warp
+            // 0's update took different paths and deadlocked in
+            // __reduce_min_sync (observed with some medium schedules).
+            const uint32_t need = __shfl_sync(0xffffffffu, S.need, 0);
             if (threadIdx.x < 32) {  // bookkeeping: warp 0 only (uniform branch)
                 const uint32_t k = threadIdx.x, qp = (t + 1) & 1u;
                 if (k >= 1 && k <= 5 && S.first_t[qp][k] != ~0u) {
@@ -1132,13 +1137,26 @@ struct MedTables {
     uint32_t n_tasks = 0;
 };
 
+// schedule constant `name`, overridable by the environment (tuning sweeps:
+// tools/med_sweep.sh)
+double med_knob(const char *name, double dflt) {
+    const char *v = std::getenv(name);
+    return v ? atof(v) : dflt;
+}
+
 MedTables build_med(const std::vector<uint32_t> &med_primes) {
     constexpr int kWarps = kThreads / 32;
     struct Desc {
         double trips;
         uint32_t x, y;
     };
-    for (double item = kItemHits; item <= kTile; item *= SQF2K_ITEM_GROWTH) {
+    const double item0 = med_knob("SQF2K_MED_ITEM", kItemHits);
+    const double growth = med_knob("SQF2K_MED_GROWTH", SQF2K_ITEM_GROWTH);
+    const double c_bucket = med_knob("SQF2K_MED_BUCKET", SQF2K_LPT_BUCKET);
+    const double c_bias = med_knob("SQF2K_MED_BIAS", SQF2K_LPT_WARP_BIAS);
+    const double c_trip = med_knob("SQF2K_MED_PER_TRIP", SQF2K_LPT_PER_TRIP);
+    const double c_task = med_knob("SQF2K_MED_TASK", SQF2K_LPT_TASK);
+    for (double item = item0; item <= kTile; item *= growth) {
         MedTables t;
         std::vector<Desc> descs;
         for (uint32_t p : med_primes) {
@@ -1162,9 +1180,9 @@ MedTables build_med(const std::vector<uint32_t> &med_primes) {
         const uint32_t n_tasks = (uint32_t)((descs.size() + 31) / 32);
         if (n_tasks > (uint32_t)(kWarps * kTaskSlots)) continue;
         std::vector<double> load(kWarps, 0.0);
-        load[kWarps - 1] = SQF2K_LPT_BUCKET;  // the bucket warp (scatter_bucket)
+        load[kWarps - 1] = c_bucket;  // the bucket warp (scatter_bucket)
         // the warp schedulers favour high warp ids: pre-charge the low ones
-        for (int w = 0; w < kWarps; ++w) load[w] += SQF2K_LPT_WARP_BIAS * (kWarps - 1 - w);
+        for (int w = 0; w < kWarps; ++w) load[w] += c_bias * (kWarps - 1 - w);
         std::vector<int> used(kWarps, 0);
         t.tasks.assign((size_t)kWarps * kTaskSlots * 64, 0u);  // step 0: idle lane
         for (uint32_t k = 0; k < n_tasks; ++k) {  // longest first, least-loaded warp with room
@@ -1172,7 +1190,7 @@ MedTables build_med(const std::vector<uint32_t> &med_primes) {
             for (int i = 0; i < kWarps; ++i)
                 if (used[i] < kTaskSlots && (w < 0 || load[i] < load[w])) w = i;
             // cost of a task: its longest lane (loop of 4 clears per trip) + overhead
-            load[w] += descs[32 * k].trips / SQF2K_LPT_PER_TRIP + SQF2K_LPT_TASK;
+            load[w] += descs[32 * k].trips / c_trip + c_task;
             const size_t at = ((size_t)w * kTaskSlots + used[w]++) * 64;
             for (uint32_t l = 0; l < 32; ++l) {
                 const uint32_t i = 32 * k + l;
@@ -1219,7 +1237,7 @@ size_t tile_smem_bytes() { return sizeof(TileSmem); }
 uint64_t bucket_hits_bound(uint64_t U, uint64_t n_bucket) { return U / 2058 + 1 + n_bucket; }
 
 template <bool FUSED, int KMAIN, bool PAT11>
-void launch_tile_as(const char *name, unsigned grid, size_t smem, const TileParams &P) {
+void launch_tile_as(const char *name, unsigned grid, size_t smem, const TileParams &P, bool pdl) {
     static bool attr = false;
     if (!attr) {
         SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<FUSED, KMAIN, PAT11>,
@@ -1231,15 +1249,22 @@ void launch_tile_as(const char *name, unsigned grid, size_t smem, const TilePara
                                         cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         attr = true;
     }
-    launch_pdl(name, tile_kernel<FUSED, KMAIN, PAT11>, dim3(grid), dim3(kThreads), smem, P);
+    launch_ex(ctx().stream, pdl, name, tile_kernel<FUSED, KMAIN, PAT11>, dim3(grid), dim3(kThreads),
+              smem, P);
 }
 
+// pdl: programmatic dependent launch (the prologue overlaps the bucket fill
+// before it on the stream).  Not for the batches of an overlapped multi-batch
+// call, whose stream predecessor is the previous batch's tile kernel: early
+// launched CTAs there measured 12-25 % slower calls in graph replays (C4:
+// 29.5 -> 33.0-36.6 ms, timing-dependent) and the bucket fill is on the side
+// stream anyway.
 template <bool FUSED, int KMAIN>
-void launch_tile(const char *name, unsigned grid, size_t smem, const TileParams &P) {
+void launch_tile(const char *name, unsigned grid, size_t smem, const TileParams &P, bool pdl) {
     if (kPattern11 && P.pat_words == pattern_words(8u))
-        launch_tile_as<FUSED, KMAIN, kPattern11>(name, grid, smem, P);
+        launch_tile_as<FUSED, KMAIN, kPattern11>(name, grid, smem, P, pdl);
     else
-        launch_tile_as<FUSED, KMAIN, false>(name, grid, smem, P);
+        launch_tile_as<FUSED, KMAIN, false>(name, grid, smem, P, pdl);
 }
 
 // Work of a batch that does not need the prime table: the medium schedule
@@ -1384,15 +1409,16 @@ void run_tile_batch(const BatchArgs &a) {
     // at least ceil(n_tiles / 2^23) CTAs: the per-thread 32-bit counters
     grid_cap = std::max<uint64_t>(grid_cap, ceil_div(n_tiles, 1ull << 23));
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(n_tiles, grid_cap));
+    const bool pdl = !a.bucket_stream;
     if (a.fused) {
         const uint32_t kmain = std::min<uint32_t>(a.k_eff, kMainMax);
-        if (kmain == 1) launch_tile<true, 1>("tile_fused", grid, smem, P);
-        else if (kmain == 2) launch_tile<true, 2>("tile_fused", grid, smem, P);
-        else if (kmain == 3) launch_tile<true, 3>("tile_fused", grid, smem, P);
-        else if (kmain == 4) launch_tile<true, 4>("tile_fused", grid, smem, P);
-        else launch_tile<true, 5>("tile_fused", grid, smem, P);
+        if (kmain == 1) launch_tile<true, 1>("tile_fused", grid, smem, P, pdl);
+        else if (kmain == 2) launch_tile<true, 2>("tile_fused", grid, smem, P, pdl);
+        else if (kmain == 3) launch_tile<true, 3>("tile_fused", grid, smem, P, pdl);
+        else if (kmain == 4) launch_tile<true, 4>("tile_fused", grid, smem, P, pdl);
+        else launch_tile<true, 5>("tile_fused", grid, smem, P, pdl);
     } else {
-        launch_tile<false, 1>("tile_export", grid, smem, P);
+        launch_tile<false, 1>("tile_export", grid, smem, P, pdl);
     }
 }
 

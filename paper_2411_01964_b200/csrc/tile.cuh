@@ -73,17 +73,19 @@ constexpr int kMaxMed = 176;            // pi(1023) - 4 = 168
 #endif
 constexpr int kTaskSlots = SQF2K_TASK_SLOTS;  // 32-lane scatter tasks per warp (registers)
 #ifndef SQF2K_ITEM_HITS
-#define SQF2K_ITEM_HITS 5
+#define SQF2K_ITEM_HITS 9.0
 #endif
-constexpr int kItemHits = SQF2K_ITEM_HITS;  // target hits per lane per tile (medium schedule)
+// target hits per lane per tile of the medium schedule (build_med); swept on
+// the C4/C5 windows with tools/med_sweep.sh: 9 (with SQF2K_LPT_WARP_BIAS
+// 0.25) 28.6 ms per C4 call against 29.5-30.0 for 3..8 and 10..16
+constexpr double kItemHits = SQF2K_ITEM_HITS;
 #ifndef SQF2K_PATTERN_11
 #define SQF2K_PATTERN_11 1
 #endif
 // p = 3, 5, 7 (and 11) are applied as one periodic word pattern: period
 // 9*25*49 words, or 9*25*49*121 with 11 (1.33 M words, 5.3 MB per copy,
 // L2-resident).  Taking 11 (541 hits per 2^16-slot tile, 27 % of the medium
-// scatter) out of the scatter measured 484.6 -> 467.7 ms per C5 call together
-// with ~5-hit descriptors; building the larger table costs ~4 us per batch,
+// scatter) out of the scatter measured 484.6 -> 467.7 ms per C5 call; building the larger table costs ~4 us per batch,
 // so domains below kPattern11MinSlots keep 11 in the scatter (C2: 0.088 vs
 // 0.092 ms per call).  SQF2K_PATTERN_11=0 never uses it.
 constexpr bool kPattern11 = SQF2K_PATTERN_11 != 0;

@@ -108,6 +108,9 @@ SmallSet small_set_upto_impl(uint64_t limit, bool with11) {
         else if (p == 5) s.present |= 2;
         else if (p == 7) s.present |= 4;
         else if (p == 11 && with11) s.present |= 8;
+#ifdef SQF2K_EXP_DROP13
+        else if (p == 13 && with11) continue;  // timing experiment only: wrong results
+#endif
         else if (p >= 11) s.med.push_back(p);
     }
     return s;
@@ -257,7 +260,8 @@ void enqueue_verify(const VerifyPlan &pl) {
     // several fused batches with fixed-capacity lists: batch b's pattern and
     // bucket lists are built on the side stream (buffer set b & 1) while batch
     // b - 1's tile kernel runs on the main stream (its tail frees the SMs)
-    const bool overlap = pl.pipeline == 0 && !pl.exact && pl.n_slots > pl.batch;
+    static const bool no_overlap = std::getenv("SQF2K_NO_OVERLAP") != nullptr;  // A/B experiments
+    const bool overlap = pl.pipeline == 0 && !pl.exact && pl.n_slots > pl.batch && !no_overlap;
     if (overlap) SQF2K_CUDA(cudaEventRecord(c.ev_primes, c.stream));
     uint64_t b = 0;
     for (uint64_t s0 = 0; s0 < pl.n_slots; s0 += pl.batch, ++b) {
@@ -364,7 +368,9 @@ void capture_graph(const VerifyPlan &pl, const uint64_t key[8]) {
     c.h2d_bytes = h2d;  // capturing copied nothing
     c.d2h_bytes = d2h;
     if (ok && graph && dev_alloc_generation() == gen &&
-        cudaGraphInstantiate(&e.exec, graph, 0) == cudaSuccess) {
+        cudaGraphInstantiate(&e.exec, graph,
+                             SQF2K_PRIORITY ? cudaGraphInstantiateFlagUseNodePriority : 0) ==
+            cudaSuccess) {
         for (auto &g : g_graphs)
             if (g.gen != gen) cudaGraphExecDestroy(g.exec);
         g_graphs.erase(std::remove_if(g_graphs.begin(), g_graphs.end(),
