@@ -45,35 +45,33 @@ constexpr uint32_t kPatStride = (kPatWordsMax + kTileWords + 3) / 4 * 4;
 // tile's words [pbase, pbase + kTileWords) never wrap.
 // First hit at or after 32g: y = (r - 32g) mod q; the word's hits are the
 // bits y, y+q, ... < 32, i.e. (bits 0, q, 2q, ...) << y.
-__global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__restrict__ table) {
-    const int NP = (present & 8u) ? 4 : 3;
-    const uint32_t q[4] = {9, 25, 49, 121};
-    const uint32_t pat[4] = {0x08040201u, 0x02000001u, 0x1u, 0x1u};
+__global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__restrict__ table,
+                               uint32_t words, uint32_t copies, uint32_t stride) {
+    const uint32_t q[5] = {9, 25, 49, 121, 169};
+    const uint32_t pat[5] = {0x08040201u, 0x02000001u, 0x1u, 0x1u, 0x1u};
     // Thread i computes words g = i, i + T, ... (T threads: a warp's stores
     // are coalesced) and steps each first-hit offset by -32T slots mod q
     // instead of dividing per word.  Word g is computed once and stored into
-    // every shifted copy: copy r (at table + r * kPatStride) holds word g at
+    // every shifted copy: copy r (at table + r * stride) holds word g at
     // index g - r, so a tile start at any pattern index has a 16-byte
-    // aligned source.
+    // aligned source (kinds 0 and 1; kind 2 has one copy of four periods).
     const uint32_t T = gridDim.x * blockDim.x, g0 = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t y[4], dec[4];
+    uint32_t y[5], dec[5];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 5; ++i) {
         const uint32_t r = (uint32_t)slot_residue(base_n, q[i]);
         y[i] = (r + q[i] - (uint32_t)((32ull * g0) % q[i])) % q[i];
         dec[i] = (uint32_t)((32ull * T) % q[i]);
     }
-    const uint32_t words = min(pattern_words(present) + kTileWords, kPatStride) + kPatCopies - 1;
-    for (uint32_t g = g0; g < words; g += T) {
+    for (uint32_t g = g0; g < words + copies - 1; g += T) {
         uint32_t clr = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            if (i < NP && ((present >> i) & 1u) && y[i] < 32) clr |= pat[i] << y[i];
+        for (int i = 0; i < 5; ++i) {
+            if (((present >> i) & 1u) && y[i] < 32) clr |= pat[i] << y[i];
             y[i] = y[i] >= dec[i] ? y[i] - dec[i] : y[i] + q[i] - dec[i];
         }
-#pragma unroll
-        for (uint32_t r = 0; r < kPatCopies; ++r)
-            if (g >= r && g - r < kPatStride) table[r * kPatStride + (g - r)] = ~clr;
+        for (uint32_t r = 0; r < copies; ++r)
+            if (g >= r && g - r < stride) table[(size_t)r * stride + (g - r)] = ~clr;
     }
 }
 
@@ -691,7 +689,7 @@ __device__ __forceinline__ void tl_tile(uint32_t i) {
 #define TLT(i) do { } while (0)
 #endif
 
-template <bool FUSED, int KMAIN, bool PAT11>
+template <bool FUSED, int KMAIN, int PAT>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TileParams P) {
     static_assert(kWordsPerThread % 4 == 0 && kThreads * kWordsPerThread == kTileWords,
                   "4-word chunks per thread");
@@ -788,9 +786,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
         // pattern index of the next tile start (t0 first; the halo has its own)
         // the period as a compile-time constant (a runtime P.pat_words
         // measured 0.5 % slower on the C5 window)
-        constexpr uint32_t pat_words = pattern_words(PAT11 ? 8u : 0u);
-        uint32_t pbase = (uint32_t)(((uint64_t)t0 * kTileWords) % pat_words);
-        const uint32_t pbase_halo = (uint32_t)((b0 / 32) % pat_words);
+        constexpr uint32_t pat_words = pattern_words(PAT == 2 ? 24u : PAT == 1 ? 8u : 0u);
+        uint32_t pbase = (uint32_t)(((uint64_t)t0 * kTileWords + P.pat_off) % pat_words);
+        const uint32_t pbase_halo = (uint32_t)((b0 / 32 + P.pat_off) % pat_words);
+        // the bulk-copy source of a tile start (16-byte aligned): kind 2 is
+        // one table of four periods (pbase stays 0 mod 4), kinds 0 and 1
+        // take the copy shifted by pbase mod 4
+        auto start_src = [&]() -> const uint32_t * {
+            if (PAT == 2) return P.pattern + pbase;
+            const uint32_t r = pbase & 3u;
+            return P.pattern + r * kPatStride + (pbase - r);
+        };
         auto start_tile = [&](uint32_t t, uint32_t at) {  // tile t's words (ring base at)
             const uint64_t tb = (uint64_t)t * kTile;
 #ifdef SQF2K_CHECKS
@@ -806,7 +812,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                 // one bulk copy (TMA) of the pattern words, from the shifted
                 // table copy that makes the source 16-byte aligned
                 if (threadIdx.x == kStarter) {
-                    const uint32_t r = pbase & 3u;
                     const uint32_t bar = smem_addr(kStartBars ? &S.start_bar[t % kRingTiles] : &S.mbar_start);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
@@ -815,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                             ring_addr + 4 * at),
-                        "l"(P.pattern + r * kPatStride + (pbase - r)), "r"((uint32_t)kTileWords * 4),
+                        "l"(start_src()), "r"((uint32_t)kTileWords * 4),
                         "r"(bar)
                         : "memory");
                     start_pending = !kStartBars;
@@ -870,11 +875,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                     init_words<kTileWords, true>(S.ring, at, tb, pbase, P);
                 } else if (kTmaStart) {
                     if (threadIdx.x == kStarter) {
-                        const uint32_t r = pbase & 3u;
                         asm volatile(
                             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                                 ring_addr + 4 * at),
-                            "l"(P.pattern + r * kPatStride + (pbase - r)),
+                            "l"(start_src()),
                             "r"((uint32_t)kTileWords * 4), "r"(smem_addr(&S.mbar_start))
                             : "memory");
                     }
@@ -1213,8 +1217,8 @@ struct MedCache {
 // one schedule per pattern kind (11 in the table or in the scatter), so
 // calls alternating between small and large domains rebuild nothing; the
 // library serialises calls
-MedCache g_med[2];
-MedCache &med_cache(const BatchArgs &a) { return g_med[(a.pattern_present >> 3) & 1u]; }
+MedCache g_med[3];
+MedCache &med_cache(const BatchArgs &a) { return g_med[pattern_kind(a.pattern_present)]; }
 
 }  // namespace
 
@@ -1236,20 +1240,20 @@ size_t tile_smem_bytes() { return sizeof(TileSmem); }
 // of (U/p^2 + 1) <= U / (2 * 1029) + n_bucket_primes.
 uint64_t bucket_hits_bound(uint64_t U, uint64_t n_bucket) { return U / 2058 + 1 + n_bucket; }
 
-template <bool FUSED, int KMAIN, bool PAT11>
+template <bool FUSED, int KMAIN, int PAT>
 void launch_tile_as(const char *name, unsigned grid, size_t smem, const TileParams &P, bool pdl) {
     static bool attr = false;
     if (!attr) {
-        SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<FUSED, KMAIN, PAT11>,
+        SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<FUSED, KMAIN, PAT>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         // carve only the shared memory kCtasPerSm CTAs need: the rest stays L1,
         // which holds the pattern table every tile reads
         const int pct = (int)((kCtasPerSm * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
-        SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<FUSED, KMAIN, PAT11>,
+        SQF2K_CUDA(cudaFuncSetAttribute(tile_kernel<FUSED, KMAIN, PAT>,
                                         cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         attr = true;
     }
-    launch_ex(ctx().stream, pdl, name, tile_kernel<FUSED, KMAIN, PAT11>, dim3(grid), dim3(kThreads),
+    launch_ex(ctx().stream, pdl, name, tile_kernel<FUSED, KMAIN, PAT>, dim3(grid), dim3(kThreads),
               smem, P);
 }
 
@@ -1261,10 +1265,15 @@ void launch_tile_as(const char *name, unsigned grid, size_t smem, const TilePara
 // stream anyway.
 template <bool FUSED, int KMAIN>
 void launch_tile(const char *name, unsigned grid, size_t smem, const TileParams &P, bool pdl) {
-    if (kPattern11 && P.pat_words == pattern_words(8u))
-        launch_tile_as<FUSED, KMAIN, kPattern11>(name, grid, smem, P, pdl);
-    else
-        launch_tile_as<FUSED, KMAIN, false>(name, grid, smem, P, pdl);
+    if (kPattern13 && P.pat_words == pattern_words(24u)) {
+        // (verify.cu selects kind 2 for fused default-depth calls only)
+        if (!FUSED || KMAIN != kMainMax) throw Error{SQF2K_ECUDA, "pattern kind 2 needs the fused main-depth kernel"};
+        launch_tile_as<FUSED, KMAIN, kPattern13 ? 2 : 0>(name, grid, smem, P, pdl);
+    } else if (kPattern11 && P.pat_words == pattern_words(8u)) {
+        launch_tile_as<FUSED, KMAIN, kPattern11 ? 1 : 0>(name, grid, smem, P, pdl);
+    } else {
+        launch_tile_as<FUSED, KMAIN, 0>(name, grid, smem, P, pdl);
+    }
 }
 
 // Work of a batch that does not need the prime table: the medium schedule
@@ -1288,14 +1297,23 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
     }
 
     // p = 3, 5, 7 pattern of this domain
-    DevBuf &pattern = a.buf ? c.pattern_b : c.pattern;
     DevBuf &counts = a.buf ? c.tile_counts_b : c.tile_counts;
-    pattern.reserve((size_t)kPatCopies * kPatStride * 4);
-    launch_on(st, "pattern", pattern_kernel,
-              dim3((unsigned)std::min<uint64_t>(ceil_div(pattern_words(a.pattern_present) + kTileWords, 256),
-                                                c.sm_count * 8)),
-              dim3(256),
-              0, a.base_n, a.pattern_present, pattern.as<uint32_t>());
+    const uint32_t pw = pattern_words(a.pattern_present);
+    if (pattern_kind(a.pattern_present) == 2) {
+        if (a.pat_off == 0) {  // once per call (later batches read it at their offset)
+            const uint32_t words = pw + kTileWords;
+            c.pattern13.reserve((size_t)words * 4);
+            launch_on(st, "pattern", pattern_kernel, dim3((unsigned)c.sm_count * 8), dim3(256), 0, a.base_n,
+                      a.pattern_present, c.pattern13.as<uint32_t>(), words, 1u, words);
+        }
+    } else {
+        DevBuf &pattern = a.buf ? c.pattern_b : c.pattern;
+        pattern.reserve((size_t)kPatCopies * kPatStride * 4);
+        launch_on(st, "pattern", pattern_kernel,
+                  dim3((unsigned)std::min<uint64_t>(ceil_div(pw + kTileWords, 256), c.sm_count * 8)), dim3(256),
+                  0, a.base_n, a.pattern_present, pattern.as<uint32_t>(),
+                  std::min(pw + kTileWords, kPatStride), (uint32_t)kPatCopies, kPatStride);
+    }
     const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);
     counts.reserve((n_bt + 1) * 4);
     SQF2K_CUDA(cudaMemsetAsync(counts.ptr, 0, (n_bt + 1) * 4, st));
@@ -1377,7 +1395,9 @@ void run_tile_batch(const BatchArgs &a) {
     P.k_max = a.k_max;
 
     P.pat_words = pattern_words(a.pattern_present);
-    P.pattern = (a.buf ? c.pattern_b : c.pattern).as<uint32_t>();
+    P.pat_off = a.pat_off;
+    P.pattern = pattern_kind(a.pattern_present) == 2 ? c.pattern13.as<uint32_t>()
+                                                      : (a.buf ? c.pattern_b : c.pattern).as<uint32_t>();
     P.med = med_cache(a).buf.as<uint32_t>();
     P.tasks = reinterpret_cast<const uint2 *>(med_cache(a).buf.as<uint32_t>() + kMaxMed);
     P.tile_start = tile_start;

@@ -92,9 +92,28 @@ constexpr bool kPattern11 = SQF2K_PATTERN_11 != 0;
 constexpr uint32_t kPatWords3 = 9 * 25 * 49;
 constexpr uint32_t kPatWordsMax = kPatWords3 * (kPattern11 ? 121 : 1);
 constexpr uint64_t kPattern11MinSlots = 1ull << 30;
-// period of the table whose present mask is `present` (bit 3: prime 11)
+// ... and 13 as well for the largest calls (SQF2K_PATTERN_13): period
+// 9*25*49*121*169 = 225.45 M words, one table per call (3.6 GB, stored as four
+// periods so that every tile start is 16-byte aligned without shifted copies,
+// read from HBM by the tile starts: 8 KB per 2^16-slot tile) and a per-batch
+// word offset; it takes the 388 hits per tile of p = 13 out of the scatter.
+#ifndef SQF2K_PATTERN_13
+#define SQF2K_PATTERN_13 1
+#endif
+constexpr bool kPattern13 = SQF2K_PATTERN_13 != 0 && kPattern11;
+constexpr uint32_t kPatPeriod13 = kPatWords3 * 121 * 169;
+#ifndef SQF2K_PATTERN_13_MIN_SLOTS
+#define SQF2K_PATTERN_13_MIN_SLOTS (1ull << 40)
+#endif
+constexpr uint64_t kPattern13MinSlots = SQF2K_PATTERN_13_MIN_SLOTS;
+// index period of the table whose present mask is `present` (bit 3: prime
+// 11, bit 4: prime 13 -- four periods, see above)
 __host__ __device__ constexpr uint32_t pattern_words(uint32_t present) {
-    return (present & 8u) ? kPatWords3 * 121 : kPatWords3;
+    return (present & 16u) ? 4 * kPatPeriod13 : (present & 8u) ? kPatWords3 * 121 : kPatWords3;
+}
+// table kind: 0 (3, 5, 7), 1 (+ 11), 2 (+ 11, 13)
+__host__ __device__ constexpr int pattern_kind(uint32_t present) {
+    return (present & 16u) ? 2 : (present & 8u) ? 1 : 0;
 }
 #ifndef SQF2K_MIN_CHUNK
 #define SQF2K_MIN_CHUNK 4
@@ -147,6 +166,7 @@ struct TileParams {
     uint32_t k_eff;      // passes inside the tile
     uint32_t k_max;      // run limit: escalate when k_max > k_eff
     uint32_t pat_words;          // period of the pattern table (pattern_words)
+    uint32_t pat_off;            // word offset of this batch in a per-call table (kind 2)
     const uint32_t *pattern;     // p = 3, 5, 7 (11) mask by u-word mod pat_words (+ kTileWords
                                  // repeated words, so a tile never wraps)
     const uint32_t *med;         // q = p^2 of the medium primes
@@ -211,7 +231,8 @@ struct BatchArgs {
     const uint32_t *primes;       // device table
     const PrimeInfo *info;        // device split
     uint64_t n_primes_bound;      // host upper bound of the table size
-    uint32_t pattern_present;     // bit i: prime 3/5/7/11 in the table
+    uint32_t pattern_present;     // bit i: prime 3/5/7/11/13 in the table
+    uint32_t pat_off;             // kind 2: word offset of this batch from the call's first
     const std::vector<uint32_t> *med_primes;
     unsigned long long *hist, *min_n, *esc, *esc_count, *fail, *fail_count;
     uint64_t esc_cap, fail_cap;

@@ -99,7 +99,7 @@ struct SmallSet {
     uint32_t present = 0;
 };
 
-SmallSet small_set_upto_impl(uint64_t limit, bool with11) {
+SmallSet small_set_upto_impl(uint64_t limit, int kind) {
     static const std::vector<uint32_t> all = small_primes(kPMed);
     SmallSet s;
     for (uint32_t p : all) {
@@ -107,24 +107,34 @@ SmallSet small_set_upto_impl(uint64_t limit, bool with11) {
         if (p == 3) s.present |= 1;
         else if (p == 5) s.present |= 2;
         else if (p == 7) s.present |= 4;
-        else if (p == 11 && with11) s.present |= 8;
+        else if (p == 11 && kind >= 1) s.present |= 8;
+        else if (p == 13 && kind >= 2) s.present |= 16;
 #ifdef SQF2K_EXP_DROP13
-        else if (p == 13 && with11) continue;  // timing experiment only: wrong results
+        else if (p == 13 && kind >= 1) continue;  // timing experiment only: wrong results
 #endif
         else if (p >= 11) s.med.push_back(p);
     }
     return s;
 }
 
-// 11 joins the pattern table for domains of kPattern11MinSlots slots or more
-SmallSet small_set_upto(uint64_t limit, uint64_t n_slots) {
-    const bool with11 = kPattern11 && n_slots >= kPattern11MinSlots;
-    if (limit >= kPMed) {  // every range above 2^20: the full set, built once
-        static const SmallSet full[2] = {small_set_upto_impl(kPMed, false),
-                                         small_set_upto_impl(kPMed, true)};
-        return full[with11];
+// The pattern table kind of a call (tile.cuh): 11 joins the table for domains
+// of kPattern11MinSlots slots or more, 13 too (one per-call table) for fused
+// main-depth calls of kPattern13MinSlots or more.
+SmallSet small_set_upto(uint64_t limit, uint64_t n_slots, bool allow13) {
+    int kind = kPattern11 && n_slots >= kPattern11MinSlots ? 1 : 0;
+    // (SQF2K_DEBUG_PAT13_MIN lowers the threshold: tests reach kind 2 on
+    // small multi-batch windows)
+    static const uint64_t min13 = [] {
+        const char *e = std::getenv("SQF2K_DEBUG_PAT13_MIN");
+        return e ? std::strtoull(e, nullptr, 0) : kPattern13MinSlots;
+    }();
+    if (kind && kPattern13 && allow13 && n_slots >= min13) kind = 2;
+    if (limit >= kPMed) {  // every range above 2^20: the full sets, built once
+        static const SmallSet full[3] = {small_set_upto_impl(kPMed, 0), small_set_upto_impl(kPMed, 1),
+                                         small_set_upto_impl(kPMed, 2)};
+        return full[kind];
     }
-    return small_set_upto_impl(limit, with11);
+    return small_set_upto_impl(limit, kind);
 }
 
 }  // namespace
@@ -216,6 +226,12 @@ void enqueue_verify(const VerifyPlan &pl) {
         a.base_n = (int64_t)A - 2 * (int64_t)H;
         a.U = H + sb;
         a.z = a.base_n < 1 ? (uint64_t)((1 - a.base_n) / 2) : 0;
+        // per-call pattern table (kind 2): this batch's words start s0 / 32
+        // words in (s0 is a multiple of the batch, hence of 128 slots, so
+        // tile starts stay 16-byte aligned)
+        a.pat_off = pattern_kind(a.pattern_present) == 2
+                        ? (uint32_t)((s0 / 32) % pattern_words(a.pattern_present))
+                        : 0u;
         if (pl.pipeline == 1) {  // two-pass: export [A - 2H, A + 2 sb), then scan it
             a.fused = false;
             a.scan_lo = 0;
@@ -404,7 +420,8 @@ int verify_range(uint64_t start, uint64_t end, uint32_t k_max, const sqf2k_verif
     pl.n_slots = (end - start) / 2;
     pl.limit = isqrt_u64(end - 1);
     pl.pipeline = o.pipeline;
-    pl.small = small_set_upto(pl.limit, pl.n_slots);
+    pl.small = small_set_upto(pl.limit, pl.n_slots,
+                              pl.pipeline == 0 && pl.k_eff >= (uint32_t)kMainMax && pl.batch % 128 == 0);
     pl.esc_cap = 1 << 16;
     pl.dev_fail_cap = std::max<uint64_t>(fail_cap, 1 << 12);
     pl.exact = (o.flags & SQF2K_EXACT_BUCKETS) != 0;

@@ -455,3 +455,33 @@ def test_smallest_exponent_matches_scan_exponents():
         smallest_exponent(4, w, 12)
     with pytest.raises(ValueError):
         smallest_exponent(11, w, 0)
+
+
+def test_pattern13_table_batches():
+    # the per-call p = 3..13 pattern table (kind 2, tile.cuh) normally serves
+    # only calls of >= 2^40 slots; SQF2K_DEBUG_PAT13_MIN lets a small
+    # multi-batch window use it, so every batch reads the table at its own
+    # word offset.  Results must equal the kind-1 path's (pinned to the
+    # reference's reports by test_run_verify_matches_large_goldens).
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import json, sys\n"
+        "from paper_2411_01964_b200.runner import verify_range\n"
+        "s, e = (1 << 50) - (1 << 34) + 1, (1 << 50) + 1\n"
+        "out = [verify_range(s, e, 30, batch_slots=b) for b in (0, 1 << 30, 1 << 28, (1 << 28) + 32)]\n"
+        "out += [verify_range(1, (1 << 33) + 1, 30, batch_slots=1 << 27)]\n"
+        "print(json.dumps([[o.histogram, o.k_sum, sorted(o.record_candidates.items())] for o in out]))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SQF2K_DEBUG_PAT13_MIN="0")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    s, e = (1 << 50) - (1 << 34) + 1, (1 << 50) + 1
+    want = verify_range(s, e, 30)
+    for g in got[:4]:
+        assert g == [want.histogram, want.k_sum, [list(x) for x in sorted(want.record_candidates.items())]]
+    base = verify_range(1, (1 << 33) + 1, 30)
+    assert got[4] == [base.histogram, base.k_sum, [list(x) for x in sorted(base.record_candidates.items())]]
