@@ -216,8 +216,15 @@ __device__ __forceinline__ uint32_t ring_base(uint32_t t) { return (t % kRingTil
 __device__ __forceinline__ uint32_t ring_back(uint32_t i, uint32_t d) {
     return i >= d ? i - d : i + kRingWords - d;
 }
-struct TileSmem {
-    uint32_t ring[kRingWords];
+// SQF2K_RING_ALIGN: the ring starts on an 8 KB boundary of the shared
+// window (the bookkeeping fields go in front, padded), so every tile buffer
+// -- and every halo, whose offset inside its buffer is a multiple of the
+// halo's byte length -- is aligned past its largest word offset and a hit's
+// word address is one LOP3 ((o >> 3) & 0x1ffc | base) instead of AND + ADD.
+#ifndef SQF2K_RING_ALIGN
+#define SQF2K_RING_ALIGN 1
+#endif
+struct TileSmemHead {
     unsigned long long first[kDepthMax + 1];
     uint32_t first_t[2][6];       // k <= 5: least tile-local slot of tile t (buffer t & 1)
     uint32_t need;                // bit k: least n with exponent k still unknown
@@ -236,12 +243,25 @@ struct TileSmem {
     uint32_t wphase[kThreads / 32];     // phases each warp has arrived on
 #endif
 };
+// dynamic shared memory starts 1 KB into the CTA's shared window (the
+// system-reserved 1 KB), so the ring lands on 8 KB at offset 7 KB
+constexpr uint32_t kSmemBase = 1024, kRingAlign = 8192;
+constexpr uint32_t kRingOffset = SQF2K_RING_ALIGN ? kRingAlign - kSmemBase : 0;
+static_assert(!SQF2K_RING_ALIGN || sizeof(TileSmemHead) <= kRingOffset, "bookkeeping fits before the ring");
+struct TileSmem : TileSmemHead {
+    uint8_t pad[SQF2K_RING_ALIGN ? kRingOffset - sizeof(TileSmemHead) : 16];
+    alignas(16) uint32_t ring[kRingWords];
+};
 
 // Clear slot o of the words starting at shared address wbase (byte address
 // of a run of words that does not wrap): one shift, one LEA, one funnel
 // shift for ~(1 << (o & 31)), one RED.
 __device__ __forceinline__ void clear_bit(uint32_t wbase, uint32_t o) {
+#if SQF2K_RING_ALIGN
+    const uint32_t addr = wbase | ((o >> 3) & 0x1ffcu);
+#else
     const uint32_t addr = wbase + ((o >> 5) << 2);
+#endif
     const uint32_t m = __funnelshift_l(0xffffffffu, 0xfffffffeu, o);
 #ifdef SQF2K_EXP_ATOMIC_AND
     atomicAnd(reinterpret_cast<uint32_t *>(__cvta_shared_to_generic(addr)), m);
@@ -726,6 +746,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     if (threadIdx.x < 12) S.first_t[threadIdx.x / 6][threadIdx.x % 6] = ~0u;
     if (threadIdx.x == 0) S.need = ~0u;
     const uint32_t ring_addr = smem_addr(S.ring);
+    if (SQF2K_RING_ALIGN && (ring_addr & (kRingAlign - 1))) __trap();  // clear_bit's OR needs it
     // per-thread counters: each adds <= 32 * kWordsPerThread = 256 per tile, and
     // run_tile_batch keeps a CTA under 2^23 tiles, so they stay below 2^31; the
     // warp sums at the end are 64-bit
