@@ -485,3 +485,29 @@ def test_pattern13_table_batches():
         assert g == [want.histogram, want.k_sum, [list(x) for x in sorted(want.record_candidates.items())]]
     base = verify_range(1, (1 << 33) + 1, 30)
     assert got[4] == [base.histogram, base.k_sum, [list(x) for x in sorted(base.record_candidates.items())]]
+
+
+@pytest.mark.parametrize("item,bias", [("3", "0"), ("16", "0.25"), ("20", "0.5")])
+def test_medium_schedules_agree(item, bias):
+    # every medium-prime schedule (build_med's knobs, read from the
+    # environment) must give the same result; items 16 and 20 once hung the
+    # tile kernel (a warp split across two phases, fixed by a warp-uniform
+    # `need`), so the subprocess runs under a timeout
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import json\n"
+        "from paper_2411_01964_b200.runner import verify_range\n"
+        "out = [verify_range((1 << 50) - (1 << 32) + 1, (1 << 50) + 1, 30),\n"
+        "       verify_range(1, (1 << 31) + 1, 30), verify_range(1, (1 << 28) + 1, 30)]\n"
+        "print(json.dumps([[o.histogram, o.k_sum, sorted(o.record_candidates.items())] for o in out]))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SQF2K_MED_ITEM=item, SQF2K_MED_BIAS=bias)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=120)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    want = [verify_range((1 << 50) - (1 << 32) + 1, (1 << 50) + 1, 30), verify_range(1, (1 << 31) + 1, 30),
+            verify_range(1, (1 << 28) + 1, 30)]
+    assert got == [[w.histogram, w.k_sum, [list(x) for x in sorted(w.record_candidates.items())]] for w in want]
