@@ -7,7 +7,8 @@ Covers the fused tile kernel and the export (bitmap) pipeline with the
 split-phase mbarrier ring at the default grid and with 1 and 3 CTAs (long
 per-CTA runs, dynamic chunks), the window scan kernels, the prime
 generators, escalation, recheck and trial division -- on [1, 2^20] and on a
-2^20-integer window ending at 2^50.  Results are checked against the oracle
+2^20-integer window ending at 2^50 -- plus the dense bucket pass and the
+per-call p <= 13 pattern table on a 2^32-integer window.  Results are checked against the oracle
 so a sanitizer run is also a parity run.
 """
 
@@ -44,6 +45,25 @@ def main() -> None:
                     assert got.record_candidates == want["record_candidates"]
             print(f"verify [{lo}, {hi}) grid {grid}: ok", flush=True)
     os.environ.pop("SQF2K_DEBUG_GRID", None)
+    # a 2^32-integer window at 2^50 in one batch: the tile-major dense bucket
+    # pass; then the same window with the per-call p <= 13 pattern table in a
+    # child process (SQF2K_DEBUG_PAT13_MIN is read once per process), in one
+    # batch and in two
+    import json
+    import subprocess
+    big = ((1 << 50) - (1 << 32) + 1, (1 << 50) + 1)
+    want = verify_range(*big, 30, batch_slots=1 << 31)
+    code = ("import json, sys\n"
+            f"sys.path.insert(0, {str(ROOT)!r})\n"
+            "from paper_2411_01964_b200.runner import verify_range\n"
+            f"out = [verify_range({big[0]}, {big[1]}, 30, batch_slots=b) for b in (1 << 31, 1 << 30)]\n"
+            "print(json.dumps([[o.histogram, sorted(o.record_candidates.items())] for o in out]))\n")
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SQF2K_DEBUG_PAT13_MIN="0"),
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    for h, c in json.loads(r.stdout.strip().splitlines()[-1]):
+        assert h == want.histogram and c == [list(x) for x in sorted(want.record_candidates.items())]
+    print(f"verify [{big[0]}, {big[1]}) dense buckets, p <= 13 table: ok", flush=True)
     # k_max = 2: failures, the failure sort and the recheck kernel
     got = verify_range(1, (1 << 16) + 1, 2)
     want = O.verify(1, (1 << 16) + 1, width=1 << 30, k_max=2)
