@@ -75,6 +75,33 @@ __global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__res
     }
 }
 
+// Kind-2 table (tile.cuh) as the AND of the p <= 11 table (period P11 words,
+// one copy) and the p = 13 words (period 169 words, in shared memory): one
+// L2 load and one store per word, where pattern_kernel spends ~25
+// instructions per word on the five residues (2.5 ms -> HBM-write-bound for
+// the 3.6 GB table).
+__global__ void pattern13_kernel(int64_t base_n, const uint32_t *__restrict__ t11, uint32_t *__restrict__ out,
+                                 uint32_t words) {
+    constexpr uint32_t P11 = kPatWords3 * 121, Q = 169;
+    __shared__ uint32_t s13[Q];
+    const uint32_t r = (uint32_t)slot_residue(base_n, Q);
+    for (uint32_t j = threadIdx.x; j < Q; j += blockDim.x) {
+        const uint32_t y = (r + Q - (32u * j) % Q) % Q;  // first hit at or after slot 32j
+        s13[j] = y < 32 ? ~(1u << y) : ~0u;
+    }
+    __syncthreads();
+    const uint32_t T = gridDim.x * blockDim.x, g0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t d11 = T % P11, d13 = T % Q;
+    uint32_t i11 = g0 % P11, i13 = g0 % Q;
+    for (uint32_t g = g0; g < words; g += T) {
+        out[g] = __ldg(t11 + i11) & s13[i13];
+        i11 += d11;
+        if (i11 >= P11) i11 -= P11;
+        i13 += d13;
+        if (i13 >= Q) i13 -= Q;
+    }
+}
+
 // -------------------------------------------------------------------------
 // Bucket pass: every hit u of a bucket prime (p >= kPMed, p^2 <= n_max) in the
 // batch domain [0, U), as a 16-bit offset in the list of bucket tile u >> kBucketShift.
@@ -1383,8 +1410,14 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
         if (a.pat_off == 0) {  // once per call (later batches read it at their offset)
             const uint32_t words = pw + kTileWords;
             c.pattern13.reserve((size_t)words * 4);
-            launch_on(st, "pattern", pattern_kernel, dim3((unsigned)c.sm_count * 8), dim3(256), 0, a.base_n,
-                      a.pattern_present, c.pattern13.as<uint32_t>(), words, 1u, words);
+            // the p <= 11 table (one copy, in the kind-1 buffer, unused by
+            // kind-2 calls), then the AND with the p = 13 words
+            const uint32_t p11 = pattern_words(8u);
+            c.pattern.reserve((size_t)kPatCopies * kPatStride * 4);
+            launch_on(st, "pattern", pattern_kernel, dim3((unsigned)ceil_div(p11, 256)), dim3(256), 0, a.base_n,
+                      a.pattern_present & 15u, c.pattern.as<uint32_t>(), p11, 1u, p11);
+            launch_on(st, "pattern13", pattern13_kernel, dim3((unsigned)c.sm_count * 8), dim3(256), 0, a.base_n,
+                      (const uint32_t *)c.pattern.as<uint32_t>(), c.pattern13.as<uint32_t>(), words);
         }
     } else {
         DevBuf &pattern = a.buf ? c.pattern_b : c.pattern;
