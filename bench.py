@@ -261,8 +261,9 @@ def measure(name: str, args, D: _Dist, rank: int, flush, stream, peak: float,
             "odd_n_per_launch": units_per_launch,
             "kernel_ms_per_launch": per_launch_ms,
             "kernel_share_of_step": (total_ms / prof_steps) / (sum(times) / len(times)),
-            "how": "per-launch CUDA events on the library stream (profile mode: PDL and "
-                   "graph replay off) over the same steps",
+            "how": "per-launch CUDA events on the launching stream (profile mode: PDL, graph "
+                   "replay and the side-stream overlap of multi-batch calls off, so each "
+                   "kernel is timed alone) over extra steps of the same call",
         },
         "kernels": {k: {"launches_per_step": v[0] / prof_steps, "ms_per_step": v[1] / prof_steps}
                     for k, v in sorted(kstats.items())},

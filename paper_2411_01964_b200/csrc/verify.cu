@@ -265,7 +265,7 @@ void enqueue_verify(const VerifyPlan &pl) {
         SQF2K_CUDA(cudaMemset(c.sched.ptr, 0, 64));
     }
     SQF2K_CUDA(cudaMemsetAsync(c.sched.ptr, 0, 64, c.side));
-    prep_tile_batch(a, c.side);
+    prep_tile_batch(a, c.profiling ? c.stream : c.side);  // (profile mode: one kernel at a time)
     generate_primes_async(pl.limit);
     a.primes = c.primes_u32.as<uint32_t>();  // (re)allocated by the generator
     a.info = c.prime_info.as<PrimeInfo>();
@@ -277,7 +277,10 @@ void enqueue_verify(const VerifyPlan &pl) {
     // bucket lists are built on the side stream (buffer set b & 1) while batch
     // b - 1's tile kernel runs on the main stream (its tail frees the SMs)
     static const bool no_overlap = std::getenv("SQF2K_NO_OVERLAP") != nullptr;  // A/B experiments
-    const bool overlap = pl.pipeline == 0 && !pl.exact && pl.n_slots > pl.batch && !no_overlap;
+    // (profile mode runs the batches without the side-stream overlap: a side
+    // kernel's events would otherwise time its wait for the SMs the tile
+    // kernel holds, not the kernel)
+    const bool overlap = pl.pipeline == 0 && !pl.exact && pl.n_slots > pl.batch && !no_overlap && !c.profiling;
     if (overlap) SQF2K_CUDA(cudaEventRecord(c.ev_primes, c.stream));
     uint64_t b = 0;
     for (uint64_t s0 = 0; s0 < pl.n_slots; s0 += pl.batch, ++b) {

@@ -1,6 +1,5 @@
 cd $GRAFT_REPO_ROOT
-python -m pytest tests/test_gpu_parity.py -x -q -k "pattern13 or large_goldens or full_range" 2>&1 | tail -2
 for r in 1 2; do
-python tools/exp_step.py experiments/lib_exp_cur.so --reps=4 2>&1 | tail -1
-python tools/exp_step.py - --reps=4 2>&1 | tail -1
+for v in cur d11 d11dyn8 dyn8 d11dyn8m2 d11dyn8s5 d11dyn16; do python tools/exp_step.py experiments/lib_exp_$v.so 1 1400000000 --reps=100 2>&1 | tail -1; done
 done
+for v in cur d11 d11dyn8; do python tools/exp_step.py experiments/lib_exp_$v.so --reps=4 2>&1 | tail -1; python tools/exp_step.py experiments/lib_exp_$v.so 1 "1<<36" --reps=20 2>&1 | tail -1; done
