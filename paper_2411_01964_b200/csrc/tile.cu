@@ -324,6 +324,11 @@ struct TileSmemHead {
     unsigned long long start_bar[kRingTiles];  // SQF2K_START_BARS: buffer b's start landed
     uint32_t last;      // this CTA finished last (epilogue)
     uint32_t chunk[2];  // the dynamic chunk just taken
+    // fixed-capacity bucket list (and the 16-byte chunk of tile counts holding
+    // its count) of the tile in ring buffer b, copied with the tile's start
+    // (SQF2K_BUCKET_PREFETCH)
+    alignas(16) uint16_t bl_hits[kRingTiles][kBucketCap];
+    alignas(16) uint32_t bl_cnt[kRingTiles][4];
 #ifdef SQF2K_CHECKS
     uint32_t tag[kRingTiles];           // tile started into each ring buffer
     uint32_t wphase[kThreads / 32];     // phases each warp has arrived on
@@ -528,6 +533,20 @@ __device__ __forceinline__ void scatter_bucket(uint32_t wbase, const TileParams 
             if (o >= skip) clear_bit(wbase, o - skip);
         }
     }
+}
+
+// scatter_bucket from the copy of tile t's list that came with its start
+// (fixed-capacity lists, kSubTiles == 1): no global-memory round trips on the
+// bucket warp's path (export kernel)
+#ifndef SQF2K_BUCKET_PREFETCH
+#define SQF2K_BUCKET_PREFETCH 1
+#endif
+constexpr bool kBucketPrefetch = SQF2K_BUCKET_PREFETCH && kSubTiles == 1;
+__device__ __forceinline__ void scatter_bucket_smem(const TileSmemHead &S, uint32_t wbase, uint32_t t,
+                                                    uint32_t b) {
+    if ((threadIdx.x >> 5) != kThreads / 32 - 1) return;
+    const uint32_t n = min(S.bl_cnt[b][t & 3u], (uint32_t)kBucketCap);
+    for (uint32_t i = threadIdx.x & 31; i < n; i += 32) clear_bit(wbase, S.bl_hits[b][i]);
 }
 
 // Start WORDS words (domain slot `base`, ring word `at`, 16-byte aligned and
@@ -904,6 +923,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             const uint32_t r = pbase & 3u;
             return P.pattern + r * kPatStride + (pbase - r);
         };
+        // main-loop starts (tiles >= t0 + 3, after the grid dependency wait)
+        // copy the tile's bucket list too; the prologue's starts cannot (the
+        // lists may still be in the making) -- sieve_tile applies the same rule
+        // (export kernel only: 3915 -> 5193 GB/s there; in the fused kernel
+        // the copies in the start transaction measured 2.4 % slower -- its
+        // starter waits for the start before arriving on the phase barrier --
+        // and a cp.async prefetch by the bucket warp 1.3 % slower)
+        const bool list_prefetch = kBucketPrefetch && !FUSED && P.tile_start == nullptr;
         auto start_tile = [&](uint32_t t, uint32_t at) {  // tile t's words (ring base at)
             const uint64_t tb = (uint64_t)t * kTile;
 #ifdef SQF2K_CHECKS
@@ -920,9 +947,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                 // table copy that makes the source 16-byte aligned
                 if (threadIdx.x == kStarter) {
                     const uint32_t bar = smem_addr(kStartBars ? &S.start_bar[t % kRingTiles] : &S.mbar_start);
+                    const bool pl = list_prefetch;  // and the tile's bucket list
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                                 "r"((uint32_t)kTileWords * 4)
+                                 "r"((uint32_t)kTileWords * 4 + (pl ? (uint32_t)kBucketCap * 2 + 16 : 0u))
                                  : "memory");
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -930,6 +958,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                         "l"(start_src()), "r"((uint32_t)kTileWords * 4),
                         "r"(bar)
                         : "memory");
+                    if (pl) {
+                        const uint32_t b = t % kRingTiles;
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                smem_addr(&S.bl_hits[b][0])),
+                            "l"(P.hits + (uint64_t)t * kBucketCap), "r"((uint32_t)kBucketCap * 2), "r"(bar)
+                            : "memory");
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                smem_addr(&S.bl_cnt[b][0])),
+                            "l"(P.tile_count + (t & ~3u)), "r"(16u), "r"(bar)
+                            : "memory");
+                    }
                     start_pending = !kStartBars;
                 }
             } else {
@@ -1097,7 +1138,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             SQF2K_CHECK(S.tag[t % kRingTiles] == t);  // its start was published
 #ifndef SQF2K_EXP_NO_SCATTER
             scatter_medium(L, ring_addr + 4 * hb, kTile);
-            scatter_bucket(ring_addr + 4 * hb, P, t, 0);
+#ifndef SQF2K_EXP_NO_BUCKET
+            if (list_prefetch && t >= t0 + 3 && !(t < ti0 || t >= ti1)) {
+                scatter_bucket_smem(S, ring_addr + 4 * hb, t, t % kRingTiles);
+            } else {
+                scatter_bucket(ring_addr + 4 * hb, P, t, 0);
+            }
+#endif
 #endif
         };
         auto next_base = [](uint32_t h) { return h + kTileWords == kRingWords ? 0u : h + kTileWords; };
@@ -1428,7 +1475,7 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
                   std::min(pw + kTileWords, kPatStride), (uint32_t)kPatCopies, kPatStride);
     }
     const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);
-    counts.reserve((n_bt + 1) * 4);
+    counts.reserve((n_bt + 4) * 4);  // (+3: the tile starts copy 16-byte chunks)
     SQF2K_CUDA(cudaMemsetAsync(counts.ptr, 0, (n_bt + 1) * 4, st));
 }
 
