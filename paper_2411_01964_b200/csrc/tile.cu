@@ -1479,6 +1479,11 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
     SQF2K_CUDA(cudaMemsetAsync(counts.ptr, 0, (n_bt + 1) * 4, st));
 }
 
+// prime-major bucket pass grid cap per SM (latency-bound chains of one unit
+// per thread: 32 measured 418.5 vs 419.9 ms per C5 call for 8)
+#ifndef SQF2K_BUCKET_GRID_PER_SM
+#define SQF2K_BUCKET_GRID_PER_SM 32
+#endif
 // bucket work units (upper bound from pi(2^m) and the table size)
 static unsigned bucket_grid(const BatchArgs &a, int j_min = 0) {
     uint64_t n_work = 0;
@@ -1490,7 +1495,7 @@ static unsigned bucket_grid(const BatchArgs &a, int j_min = 0) {
         n_work += (hi - pi2[j]) * ((a.U + (1ull << sh) - 1) >> sh);
     }
     return (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>(ceil_div(n_work, 256), (uint64_t)ctx().sm_count * 8));
+        1, std::min<uint64_t>(ceil_div(n_work, 256), (uint64_t)ctx().sm_count * SQF2K_BUCKET_GRID_PER_SM));
 }
 
 // Fixed-capacity bucket lists of a batch on stream st (after its prep and
