@@ -144,7 +144,10 @@ void launch_ex(cudaStream_t st, bool pdl, const char *name, void (*kernel)(KArgs
     }
     cfg.attrs = attr;
     cfg.numAttrs = n;
-    SQF2K_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+    if (e != cudaSuccess)  // (with CUDA_LAUNCH_BLOCKING=1: this kernel's own fault)
+        throw Error{e == cudaErrorMemoryAllocation ? SQF2K_ENOMEM : SQF2K_ECUDA,
+                    std::string("launch of ") + name + ": " + cudaGetErrorString(e)};
     if (c.profiling) {
         SQF2K_CUDA(cudaEventRecord(b, st));
         c.pending.push_back({c.stat_index(name), a, b});

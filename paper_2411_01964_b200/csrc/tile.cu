@@ -192,9 +192,12 @@ __global__ void __launch_bounds__(256) bucket_kernel(
         // <= 5 hits (q >= 2^(20+2j), range 2^(22+2j)): all atomics in flight
         // together, then the stores -- one round trip, not one per hit
         const uint64_t u0 = lo + (r >= lm ? r - lm : r + q - lm);
+        // hits u0 + i q < hi, compared as i q < hi - u0: u0 + i q itself can
+        // pass 2^64 near the domain top (q < 2^62, so 4 q does not)
+        const uint64_t span = u0 < hi ? hi - u0 : 0;
         int nh = 0;
 #pragma unroll
-        for (int i = 0; i < 5; ++i) nh += (u0 + (uint64_t)i * q < hi) ? 1 : 0;
+        for (int i = 0; i < 5; ++i) nh += ((uint64_t)i * q < span) ? 1 : 0;
         uint32_t hu[5], pos[5];
         uint32_t bt[5];
 #pragma unroll

@@ -511,3 +511,17 @@ def test_medium_schedules_agree(item, bias):
     want = [verify_range((1 << 50) - (1 << 32) + 1, (1 << 50) + 1, 30), verify_range(1, (1 << 31) + 1, 30),
             verify_range(1, (1 << 28) + 1, 30)]
     assert got == [[w.histogram, w.k_sum, [list(x) for x in sorted(w.record_candidates.items())]] for w in want]
+
+
+def test_domain_top_large_window():
+    # a 2^40-integer window just below 2^62 (the domain's top): bucket primes
+    # up to 2^31 with q = p^2 near 2^62, where u0 + 4q passes 2^64 -- the
+    # bucket pass once counted such wrapped positions as hits (an illegal
+    # address); pipelines, bucket modes and batch sizes must agree, and
+    # every odd n must be counted once
+    s, e = (1 << 62) - (1 << 40) + 1, (1 << 62) - 1
+    base = verify_range(s, e, 30)
+    assert base.odd_scanned == (e - s) // 2
+    assert not base.failures
+    for kw in [dict(pipeline="bitmap"), dict(exact_buckets=True), dict(batch_slots=1 << 36)]:
+        assert verify_range(s, e, 30, **kw) == base, kw
