@@ -449,7 +449,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t pari
 #define SQF2K_SCAN_CHUNK 4
 #endif
 #ifndef SQF2K_LPT_BUCKET
-#define SQF2K_LPT_BUCKET 8.0  // (4: C5 420.1 ms, 8: 418.7; C4 26.84 vs 26.74)
+#define SQF2K_LPT_BUCKET 8.0  // fixed bucket warp's pre-charge (4 -> 8 measured C5 420.1 -> 418.7 ms)
 #define SQF2K_LPT_PER_TRIP 2.0
 #define SQF2K_LPT_TASK 2.0
 #endif
@@ -513,12 +513,23 @@ __device__ __forceinline__ void init_medium(MedLane &L, const TileParams &P, uin
     }
 }
 
+// The bucket hits of a tile are cleared by one warp: a fixed last warp with a
+// lighter medium share (SQF2K_LPT_BUCKET), or -- for the kind-2 calls (>= 2^40
+// slots) -- warp t mod 8 with an even share: measured C5 418.6 -> 415.8 ms,
+// while C3, C4 and the export kernel were 0.4-1.6 % faster with the fixed warp.
+// SQF2K_BUCKET_ROTATE=0 keeps the fixed warp everywhere.
+#ifndef SQF2K_BUCKET_ROTATE
+#define SQF2K_BUCKET_ROTATE 1
+#endif
+template <int PAT>
+__device__ __forceinline__ constexpr bool bucket_rotates() { return SQF2K_BUCKET_ROTATE && PAT == 2; }
 // clear the bucket hits of tile t with offsets in [skip, kTile), shifted by
-// -skip (its kSubTiles bucket-tile lists); run by the last warp only (~9
+// -skip (its kSubTiles bucket-tile lists); run by one warp (~9
 // hits per 2^16 slots; build_med gives that warp less medium work)
+template <bool ROTATE>
 __device__ __forceinline__ void scatter_bucket(uint32_t wbase, const TileParams &P, uint32_t t,
                                                uint32_t skip) {
-    if ((threadIdx.x >> 5) != kThreads / 32 - 1) return;
+    if ((threadIdx.x >> 5) != (ROTATE ? t & (kThreads / 32 - 1) : kThreads / 32 - 1)) return;
 #pragma unroll
     for (int j = 0; j < kSubTiles; ++j) {
         const uint32_t bt = t * kSubTiles + j;
@@ -1054,7 +1065,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
                 scatter_medium(L, ring_addr + 4 * halo_at, H);
                 if (!waited) grid_dependency_wait();  // bucket lists from here on
                 waited = true;
-                scatter_bucket(ring_addr + 4 * halo_at, P, t0 - 1, kTile - H);
+                scatter_bucket<bucket_rotates<PAT>()>(ring_addr + 4 * halo_at, P, t0 - 1, kTile - H);
             } else {
                 for (uint32_t i = threadIdx.x; i < HW; i += kThreads) S.ring[halo_at + i] = 0u;
             }
@@ -1145,7 +1156,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             if (list_prefetch && t >= t0 + 3 && !(t < ti0 || t >= ti1)) {
                 scatter_bucket_smem(S, ring_addr + 4 * hb, t, t % kRingTiles);
             } else {
-                scatter_bucket(ring_addr + 4 * hb, P, t, 0);
+                scatter_bucket<bucket_rotates<PAT>()>(ring_addr + 4 * hb, P, t, 0);
             }
 #endif
 #endif
@@ -1305,7 +1316,7 @@ double med_knob(const char *name, double dflt) {
     return v ? atof(v) : dflt;
 }
 
-MedTables build_med(const std::vector<uint32_t> &med_primes) {
+MedTables build_med(const std::vector<uint32_t> &med_primes, bool rotate) {
     constexpr int kWarps = kThreads / 32;
     struct Desc {
         double trips;
@@ -1313,7 +1324,7 @@ MedTables build_med(const std::vector<uint32_t> &med_primes) {
     };
     const double item0 = med_knob("SQF2K_MED_ITEM", kItemHits);
     const double growth = med_knob("SQF2K_MED_GROWTH", SQF2K_ITEM_GROWTH);
-    const double c_bucket = med_knob("SQF2K_MED_BUCKET", SQF2K_LPT_BUCKET);
+    const double c_bucket = rotate ? 0.0 : med_knob("SQF2K_MED_BUCKET", SQF2K_LPT_BUCKET);
     const double c_bias = med_knob("SQF2K_MED_BIAS", SQF2K_LPT_WARP_BIAS);
     const double c_trip = med_knob("SQF2K_MED_PER_TRIP", SQF2K_LPT_PER_TRIP);
     const double c_task = med_knob("SQF2K_MED_TASK", SQF2K_LPT_TASK);
@@ -1443,7 +1454,7 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
     constexpr size_t kTaskWords = (size_t)(kThreads / 32) * kTaskSlots * 64;
     MedCache &med = med_cache(a);
     if (med.key != *a.med_primes || !med.buf.ptr) {
-        MedTables t = build_med(*a.med_primes);
+        MedTables t = build_med(*a.med_primes, SQF2K_BUCKET_ROTATE && pattern_kind(a.pattern_present) == 2);
         med.key = *a.med_primes;
         med.buf.reserve((kMaxMed + kTaskWords) * 4);
         std::vector<uint32_t> host(kMaxMed + kTaskWords, 0);
