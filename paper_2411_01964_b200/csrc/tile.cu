@@ -845,8 +845,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
     const bool dynamic = P.n_tiles >= (uint64_t)kDynMinTiles * G;
     const uint32_t S1 = (uint32_t)((uint64_t)P.n_tiles * kStaticEighths / (8ull * G));
     const uint32_t dyn0 = dynamic ? S1 * G : P.n_tiles;  // first dynamically scheduled tile
-    // dynamic chunks of ~1/(8G) of the rest: an atomicAdd each, no CAS races
-    const uint32_t csz = max((P.n_tiles - dyn0) / (8 * G), (uint32_t)kMinChunk);
+    // dynamic chunks (sizes below): an atomicAdd each, no CAS races
+// dynamic chunks of ~1/(6G) of the dynamic tiles, the last G chunks' worth
+// handed out at half size (measured on C5: 415.8 -> 413.7 ms; a chunk's
+// start-up -- halo, descriptor offsets, pipeline fill -- costs ~3 us, so
+// smaller chunks throughout were slower: /16 417.4, /32 422.2 ms)
+#ifndef SQF2K_CHUNK_DIV
+#define SQF2K_CHUNK_DIV 6
+#endif
+#ifndef SQF2K_TAPER
+#define SQF2K_TAPER 2
+#endif
+#ifndef SQF2K_TAPER_TAIL
+#define SQF2K_TAPER_TAIL 1
+#endif
+    const uint32_t csz = max((P.n_tiles - dyn0) / (SQF2K_CHUNK_DIV * G), (uint32_t)kMinChunk);
     uint32_t t0 = dynamic ? S1 * blockIdx.x : (uint32_t)((uint64_t)P.n_tiles * blockIdx.x / G);
     uint32_t t1 = dynamic ? t0 + S1 : (uint32_t)((uint64_t)P.n_tiles * (blockIdx.x + 1) / G);
     const uint32_t H = FUSED ? P.H : 0u;
@@ -909,9 +922,27 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) tile_kernel(const TilePa
             __syncthreads();  // the last chunk's drain is done with the ring
             if (threadIdx.x == 0) {
                 const uint32_t k = atomicAdd(&P.sched[0], 1u);
+#if SQF2K_TAPER
+                // tapered tail: the last ~G * csz tiles go out in chunks of
+                // csz / SQF2K_TAPER, so the CTAs finish closer together
+                const uint64_t D = P.n_tiles - dyn0, tail = (uint64_t)SQF2K_TAPER_TAIL * G * csz;
+                const uint64_t n_big = D > tail ? (D - tail) / csz : 0;
+                const uint32_t small = max(csz / SQF2K_TAPER, (uint32_t)kMinChunk);
+                uint64_t lo, sz;
+                if (k < n_big) {
+                    lo = (uint64_t)dyn0 + (uint64_t)k * csz;
+                    sz = csz;
+                } else {
+                    lo = (uint64_t)dyn0 + n_big * csz + (uint64_t)(k - n_big) * small;
+                    sz = small;
+                }
+                S.chunk[0] = (uint32_t)min(lo, (uint64_t)P.n_tiles);
+                S.chunk[1] = (uint32_t)min(lo + sz, (uint64_t)P.n_tiles);
+#else
                 const uint64_t lo = (uint64_t)dyn0 + (uint64_t)k * csz;
                 S.chunk[0] = (uint32_t)min(lo, (uint64_t)P.n_tiles);
                 S.chunk[1] = (uint32_t)min(lo + csz, (uint64_t)P.n_tiles);
+#endif
             }
             __syncthreads();
             t0 = S.chunk[0];
