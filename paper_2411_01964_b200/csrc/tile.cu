@@ -1353,14 +1353,15 @@ MedTables build_med(const std::vector<uint32_t> &med_primes, bool rotate) {
         double trips;
         uint32_t x, y;
     };
-    // (kind-2 calls, rotating bucket warp: 7.5 hits measured best, C5 410.4
-    // ms against 411.1 for 6 and 8 and 413.7 for 9)
+    // kind-2 calls (rotating bucket warp): constants from a random search over
+    // item / bias / per-trip / per-task on C5 (experiments: 41 schedules,
+    // 407.8 ms best against 410.4 for the best item-only choice, 7.5 hits)
     const double item0 = med_knob("SQF2K_MED_ITEM", rotate ? kItemHitsRotate : kItemHits);
     const double growth = med_knob("SQF2K_MED_GROWTH", SQF2K_ITEM_GROWTH);
     const double c_bucket = rotate ? 0.0 : med_knob("SQF2K_MED_BUCKET", SQF2K_LPT_BUCKET);
-    const double c_bias = med_knob("SQF2K_MED_BIAS", SQF2K_LPT_WARP_BIAS);
+    const double c_bias = med_knob("SQF2K_MED_BIAS", rotate ? 0.75 : SQF2K_LPT_WARP_BIAS);
     const double c_trip = med_knob("SQF2K_MED_PER_TRIP", SQF2K_LPT_PER_TRIP);
-    const double c_task = med_knob("SQF2K_MED_TASK", SQF2K_LPT_TASK);
+    const double c_task = med_knob("SQF2K_MED_TASK", rotate ? 0.0 : SQF2K_LPT_TASK);
     for (double item = item0; item <= kTile; item *= growth) {
         MedTables t;
         std::vector<Desc> descs;

@@ -79,7 +79,7 @@ constexpr int kTaskSlots = SQF2K_TASK_SLOTS;  // 32-lane scatter tasks per warp 
 // the C4/C5 windows with tools/med_sweep.sh: 9 (with SQF2K_LPT_WARP_BIAS
 // 0.25) 28.6 ms per C4 call against 29.5-30.0 for 3..8 and 10..16
 constexpr double kItemHits = SQF2K_ITEM_HITS;
-constexpr double kItemHitsRotate = 7.5;  // the same for the kind-2 schedule (tile.cu)
+constexpr double kItemHitsRotate = 6.24;  // the same for the kind-2 schedule (tile.cu)
 #ifndef SQF2K_PATTERN_11
 #define SQF2K_PATTERN_11 1
 #endif
