@@ -514,7 +514,7 @@ __device__ __forceinline__ void init_medium(MedLane &L, const TileParams &P, uin
 }
 
 // The bucket hits of a tile are cleared by one warp: a fixed last warp with a
-// lighter medium share (SQF2K_LPT_BUCKET), or -- for the kind-2 calls (>= 2^40
+// lighter medium share (SQF2K_LPT_BUCKET), or -- for the kind-2 calls (>= 2^39
 // slots) -- warp t mod 8 with an even share: measured C5 418.6 -> 415.8 ms,
 // while C3, C4 and the export kernel were 0.4-1.6 % faster with the fixed warp.
 // SQF2K_BUCKET_ROTATE=0 keeps the fixed warp everywhere.

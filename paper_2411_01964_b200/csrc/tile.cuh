@@ -104,7 +104,7 @@ constexpr uint64_t kPattern11MinSlots = 1ull << 30;
 constexpr bool kPattern13 = SQF2K_PATTERN_13 != 0 && kPattern11;
 constexpr uint32_t kPatPeriod13 = kPatWords3 * 121 * 169;
 #ifndef SQF2K_PATTERN_13_MIN_SLOTS
-#define SQF2K_PATTERN_13_MIN_SLOTS (1ull << 40)
+#define SQF2K_PATTERN_13_MIN_SLOTS (1ull << 39)  // (C4, 2^39 slots: 26.70 -> 26.54 ms with kind 2)
 #endif
 constexpr uint64_t kPattern13MinSlots = SQF2K_PATTERN_13_MIN_SLOTS;
 // index period of the table whose present mask is `present` (bit 3: prime
