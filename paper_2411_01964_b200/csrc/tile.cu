@@ -45,34 +45,63 @@ constexpr uint32_t kPatStride = (kPatWordsMax + kTileWords + 3) / 4 * 4;
 // tile's words [pbase, pbase + kTileWords) never wrap.
 // First hit at or after 32g: y = (r - 32g) mod q; the word's hits are the
 // bits y, y+q, ... < 32, i.e. (bits 0, q, 2q, ...) << y.
-__global__ void pattern_kernel(int64_t base_n, uint32_t present, uint32_t *__restrict__ table,
+struct PatResidues {
+    uint32_t r[5];  // slot_residue(base_n, q) for q = 9, 25, 49, 121, 169 (host-computed)
+};
+
+__global__ void pattern_kernel(PatResidues res, uint32_t present, uint32_t *__restrict__ table,
                                uint32_t words, uint32_t copies, uint32_t stride) {
-    const uint32_t q[5] = {9, 25, 49, 121, 169};
+    constexpr uint32_t q[5] = {9, 25, 49, 121, 169};
     const uint32_t pat[5] = {0x08040201u, 0x02000001u, 0x1u, 0x1u, 0x1u};
-    // Thread i computes words g = i, i + T, ... (T threads: a warp's stores
-    // are coalesced) and steps each first-hit offset by -32T slots mod q
-    // instead of dividing per word.  Word g is computed once and stored into
-    // every shifted copy: copy r (at table + r * stride) holds word g at
-    // index g - r, so a tile start at any pattern index has a 16-byte
-    // aligned source (kinds 0 and 1; kind 2 has one copy of four periods).
-    const uint32_t T = gridDim.x * blockDim.x, g0 = blockIdx.x * blockDim.x + threadIdx.x;
+    // Copy r (at table + r * stride, copies <= 4) holds word g at index g - r,
+    // so a tile start at any pattern index has a 16-byte aligned source
+    // (kinds 0 and 1; kind 2 has one copy of four periods).  Thread i builds
+    // the aligned 4-word chunks c = i, i + T, ... of every copy: words 4c ..
+    // 4c + 6 once, then one 16-byte store per copy (chunk c of copy r is
+    // words 4c + r .. 4c + r + 3).  First-hit offsets step by -32 slots per
+    // word and by -128T per chunk, mod q; the residues of base_n come from
+    // the host, the per-thread offsets are 32-bit constant-divisor
+    // remainders (the 64-bit remainders and the scalar stores of the first
+    // version took 14 us for the kind-1 table, now ~5).
+    const uint32_t T = gridDim.x * blockDim.x, c0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t n_chunks = (words + 3) / 4;
     uint32_t y[5], dec[5];
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-        const uint32_t r = (uint32_t)slot_residue(base_n, q[i]);
-        y[i] = (r + q[i] - (uint32_t)((32ull * g0) % q[i])) % q[i];
-        dec[i] = (uint32_t)((32ull * T) % q[i]);
+        const uint32_t off = (128u * (c0 % q[i])) % q[i];  // 32 * 4 c0 mod q
+        y[i] = (res.r[i] + q[i] - off) % q[i];
+        dec[i] = (128u * (T % q[i])) % q[i];
     }
-    for (uint32_t g = g0; g < words + copies - 1; g += T) {
-        uint32_t clr = 0;
+    for (uint32_t c = c0; c < n_chunks; c += T) {
+        uint32_t w[7], yy[5];
 #pragma unroll
-        for (int i = 0; i < 5; ++i) {
-            if (((present >> i) & 1u) && y[i] < 32) clr |= pat[i] << y[i];
-            y[i] = y[i] >= dec[i] ? y[i] - dec[i] : y[i] + q[i] - dec[i];
+        for (int i = 0; i < 5; ++i) yy[i] = y[i];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+            uint32_t clr = 0;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const uint32_t d1 = 32u % q[i];
+                if (((present >> i) & 1u) && yy[i] < 32) clr |= pat[i] << yy[i];
+                yy[i] = yy[i] >= d1 ? yy[i] - d1 : yy[i] + q[i] - d1;
+            }
+            w[k] = ~clr;
         }
-        for (uint32_t r = 0; r < copies; ++r)
-            if (g >= r && g - r < stride) table[(size_t)r * stride + (g - r)] = ~clr;
+#pragma unroll
+        for (uint32_t r = 0; r < 4; ++r)
+            if (r < copies)
+                *reinterpret_cast<uint4 *>(table + (size_t)r * stride + 4ull * c) =
+                    make_uint4(w[r], w[r + 1], w[r + 2], w[r + 3]);
+#pragma unroll
+        for (int i = 0; i < 5; ++i) y[i] = y[i] >= dec[i] ? y[i] - dec[i] : y[i] + q[i] - dec[i];
     }
+}
+
+PatResidues pat_residues(int64_t base_n) {
+    PatResidues p;
+    const uint64_t q[5] = {9, 25, 49, 121, 169};
+    for (int i = 0; i < 5; ++i) p.r[i] = (uint32_t)slot_residue(base_n, q[i]);
+    return p;
 }
 
 // Kind-2 table (tile.cuh) as the AND of the p <= 11 table (period P11 words,
@@ -424,12 +453,20 @@ __device__ __forceinline__ void phase_wait(unsigned long long *bar, uint32_t pha
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
     uint32_t done = 0;
     for (;;) {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; "
-            "selp.u32 %0, 1, 0, p; }"
-            : "=r"(done)
-            : "r"(smem_addr(bar)), "r"(parity), "r"(kWaitHintNs)
-            : "memory");
+        if (kWaitHintNs)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; "
+                "selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(smem_addr(bar)), "r"(parity), "r"(kWaitHintNs)
+                : "memory");
+        else  // (the system-dependent suspend limit)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+                "selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(smem_addr(bar)), "r"(parity)
+                : "memory");
         if (done) break;
         if (kWaitSleepNs) __nanosleep(kWaitSleepNs);  // leave the issue slots to working warps
     }
@@ -807,7 +844,7 @@ __device__ __forceinline__ void tl_mark(int i) {
     if (threadIdx.x != 0 || blockIdx.x >= 4096) return;
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_timeline[blockIdx.x][i] = t;
+    g_timeline[blockIdx.x][i] = t & ((1ull << 56) - 1);  // (bits 56+ carry the SM id in [0])
     if (i == 3) {
         unsigned sm;
         asm("mov.u32 %0, %%smid;" : "=r"(sm));
@@ -1509,7 +1546,7 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
             // kind-2 calls), then the AND with the p = 13 words
             const uint32_t p11 = pattern_words(8u);
             c.pattern.reserve((size_t)kPatCopies * kPatStride * 4);
-            launch_on(st, "pattern", pattern_kernel, dim3((unsigned)ceil_div(p11, 256)), dim3(256), 0, a.base_n,
+            launch_on(st, "pattern", pattern_kernel, dim3((unsigned)ceil_div(p11, 1024)), dim3(256), 0, pat_residues(a.base_n),
                       a.pattern_present & 15u, c.pattern.as<uint32_t>(), p11, 1u, p11);
             launch_on(st, "pattern13", pattern13_kernel, dim3((unsigned)c.sm_count * 8), dim3(256), 0, a.base_n,
                       (const uint32_t *)c.pattern.as<uint32_t>(), c.pattern13.as<uint32_t>(), words);
@@ -1518,8 +1555,8 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
         DevBuf &pattern = a.buf ? c.pattern_b : c.pattern;
         pattern.reserve((size_t)kPatCopies * kPatStride * 4);
         launch_on(st, "pattern", pattern_kernel,
-                  dim3((unsigned)std::min<uint64_t>(ceil_div(pw + kTileWords, 256), c.sm_count * 8)), dim3(256),
-                  0, a.base_n, a.pattern_present, pattern.as<uint32_t>(),
+                  dim3((unsigned)std::min<uint64_t>(ceil_div(pw + kTileWords, 1024), c.sm_count * 8)), dim3(256),
+                  0, pat_residues(a.base_n), a.pattern_present, pattern.as<uint32_t>(),
                   std::min(pw + kTileWords, kPatStride), (uint32_t)kPatCopies, kPatStride);
     }
     const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);

@@ -92,7 +92,10 @@ constexpr double kItemHitsRotate = 6.24;  // the same for the kind-2 schedule (t
 constexpr bool kPattern11 = SQF2K_PATTERN_11 != 0;
 constexpr uint32_t kPatWords3 = 9 * 25 * 49;
 constexpr uint32_t kPatWordsMax = kPatWords3 * (kPattern11 ? 121 : 1);
-constexpr uint64_t kPattern11MinSlots = 1ull << 30;
+#ifndef SQF2K_PATTERN_11_MIN_SLOTS
+#define SQF2K_PATTERN_11_MIN_SLOTS (1ull << 30)
+#endif
+constexpr uint64_t kPattern11MinSlots = SQF2K_PATTERN_11_MIN_SLOTS;
 // ... and 13 as well for the largest calls (SQF2K_PATTERN_13): period
 // 9*25*49*121*169 = 225.45 M words, one table per call (3.6 GB, stored as four
 // periods so that every tile start is 16-byte aligned without shifted copies,
