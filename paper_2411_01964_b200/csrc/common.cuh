@@ -93,7 +93,10 @@ struct Context {
     DevBuf acc, esc, fail, fail_sorted, window, kvals, bits_out, host_primes;
     DevBuf pattern, prime_info, sched;
     DevBuf pattern_b, tile_counts_b, hits_b;  // second buffer set (batch parity 1)
-    DevBuf pattern13;                         // per-call table with 11 and 13 (tile.cuh)
+    DevBuf pattern13;                         // wheel table with 11 and 13 (tile.cuh)
+    // present mask of the wheel table held by pattern (kind 0), pattern_b
+    // (kind 1) and pattern13 (kind 2); ~0u: not built
+    uint32_t wheel_present[3] = {~0u, ~0u, ~0u};
     void *pinned = nullptr;  // small pinned host staging (summary readback)
     uint64_t h2d_bytes = 0, d2h_bytes = 0;  // copy accounting (bench e2e)
     uint64_t primes_limit = 0;  // primes_u32 holds all primes <= primes_limit

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <tuple>
 #include <vector>
 
 #include "collectives.cuh"
@@ -1515,6 +1516,66 @@ void launch_tile(const char *name, unsigned grid, size_t smem, const TileParams 
     }
 }
 
+// Wheel tables.  The pattern words of a domain whose slot 0 is the odd n =
+// base depend on base only through its residues mod q = 9, 25, 49 (121,
+// 169), and a shift by one word (32 slots = 64 in n) steps every residue by
+// 64, a unit mod their product Q: the table of base is the table of base 1
+// read d words in, d = (base - 1) / 64 mod Q.  So each kind has one table,
+// built for base 1 the first time a call needs it (kind 2: 3.6 GB, ~1 ms)
+// and read by every later batch at its own offset.
+uint64_t inv_mod(uint64_t a, uint64_t m) {  // a^-1 mod m (gcd(a, m) = 1)
+    int64_t t = 0, nt = 1, r = (int64_t)m, nr = (int64_t)(a % m);
+    while (nr) {
+        const int64_t q = r / nr;
+        std::tie(t, nt) = std::make_pair(nt, t - q * nt);
+        std::tie(r, nr) = std::make_pair(nr, r - q * nr);
+    }
+    return (uint64_t)(t < 0 ? t + (int64_t)m : t);
+}
+
+uint32_t wheel_offset(int64_t base_n, uint32_t present) {
+    const int kind = pattern_kind(present);
+    const uint64_t Q = kind == 2 ? kPatPeriod13 : pattern_words(present);
+    static const uint64_t inv[3] = {inv_mod(64, kPatWords3), inv_mod(64, kPatWords3 * 121ull),
+                                    inv_mod(64, kPatPeriod13)};
+    const int64_t diff = (base_n - 1) % (int64_t)Q;
+    const uint64_t d = (uint64_t)(diff < 0 ? diff + (int64_t)Q : diff) * inv[kind] % Q;
+    if (kind != 2) return (uint32_t)d;
+    // kind 2 (four periods, no shifted copies): the d' = d mod Q that is 0
+    // mod 4 keeps every tile start 16-byte aligned
+    uint64_t e = d;
+    while (e & 3u) e += Q;
+    return (uint32_t)e;
+}
+
+void ensure_wheel(int kind, uint32_t present, cudaStream_t st) {
+    Context &c = ctx();
+    if (c.wheel_present[kind] == present) return;
+    const PatResidues base1 = pat_residues(1);
+    if (kind == 2) {
+        // the p <= 11 table (kind 1) first, then its AND with the p = 13 words
+        ensure_wheel(1, present & 15u, st);
+        const uint32_t words = pattern_words(present) + kTileWords;
+        c.pattern13.reserve((size_t)words * 4);
+        c.wheel_present[2] = ~0u;
+        launch_on(st, "pattern13", pattern13_kernel, dim3((unsigned)c.sm_count * 8), dim3(256), 0, (int64_t)1,
+                  (const uint32_t *)c.pattern_b.as<uint32_t>(), c.pattern13.as<uint32_t>(), words);
+    } else {
+        // kPatCopies shifted copies (a tile start at any index has a 16-byte
+        // aligned source), each a period plus a tile so that no start wraps
+        DevBuf &t = kind == 1 ? c.pattern_b : c.pattern;
+        const uint32_t pw = pattern_words(present);
+        t.reserve((size_t)kPatCopies * kPatStride * 4);
+        c.wheel_present[kind] = ~0u;
+        launch_on(st, "pattern", pattern_kernel,
+                  dim3((unsigned)std::min<uint64_t>(ceil_div(pw + kTileWords, 1024), c.sm_count * 8)), dim3(256),
+                  0, base1, present, t.as<uint32_t>(), std::min(pw + kTileWords, kPatStride),
+                  (uint32_t)kPatCopies, kPatStride);
+    }
+    c.wheel_present[kind] = present;
+    dev_alloc_bump();  // captured graphs read the tables: a rebuilt one retires them
+}
+
 // Work of a batch that does not need the prime table: the medium schedule
 // (host-built, cached), the p = 3, 5, 7 pattern and the bucket counters --
 // on stream `st` (the side stream for the first batch of a call).
@@ -1535,30 +1596,10 @@ void prep_tile_batch(const BatchArgs &a, cudaStream_t st) {
         dev_alloc_bump();  // captured graphs read this table
     }
 
-    // p = 3, 5, 7 pattern of this domain
+    // the wheel table of this kind (built once per context: its words depend
+    // only on the primes in it; a batch reads it at wheel_offset)
     DevBuf &counts = a.buf ? c.tile_counts_b : c.tile_counts;
-    const uint32_t pw = pattern_words(a.pattern_present);
-    if (pattern_kind(a.pattern_present) == 2) {
-        if (a.pat_off == 0) {  // once per call (later batches read it at their offset)
-            const uint32_t words = pw + kTileWords;
-            c.pattern13.reserve((size_t)words * 4);
-            // the p <= 11 table (one copy, in the kind-1 buffer, unused by
-            // kind-2 calls), then the AND with the p = 13 words
-            const uint32_t p11 = pattern_words(8u);
-            c.pattern.reserve((size_t)kPatCopies * kPatStride * 4);
-            launch_on(st, "pattern", pattern_kernel, dim3((unsigned)ceil_div(p11, 1024)), dim3(256), 0, pat_residues(a.base_n),
-                      a.pattern_present & 15u, c.pattern.as<uint32_t>(), p11, 1u, p11);
-            launch_on(st, "pattern13", pattern13_kernel, dim3((unsigned)c.sm_count * 8), dim3(256), 0, a.base_n,
-                      (const uint32_t *)c.pattern.as<uint32_t>(), c.pattern13.as<uint32_t>(), words);
-        }
-    } else {
-        DevBuf &pattern = a.buf ? c.pattern_b : c.pattern;
-        pattern.reserve((size_t)kPatCopies * kPatStride * 4);
-        launch_on(st, "pattern", pattern_kernel,
-                  dim3((unsigned)std::min<uint64_t>(ceil_div(pw + kTileWords, 1024), c.sm_count * 8)), dim3(256),
-                  0, pat_residues(a.base_n), a.pattern_present, pattern.as<uint32_t>(),
-                  std::min(pw + kTileWords, kPatStride), (uint32_t)kPatCopies, kPatStride);
-    }
+    ensure_wheel(pattern_kind(a.pattern_present), a.pattern_present, st);
     const uint32_t n_bt = (uint32_t)ceil_div(a.U, kBucketTile);
     counts.reserve((n_bt + 4) * 4);  // (+3: the tile starts copy 16-byte chunks)
     SQF2K_CUDA(cudaMemsetAsync(counts.ptr, 0, (n_bt + 1) * 4, st));
@@ -1652,9 +1693,10 @@ void run_tile_batch(const BatchArgs &a) {
     P.k_max = a.k_max;
 
     P.pat_words = pattern_words(a.pattern_present);
-    P.pat_off = a.pat_off;
-    P.pattern = pattern_kind(a.pattern_present) == 2 ? c.pattern13.as<uint32_t>()
-                                                      : (a.buf ? c.pattern_b : c.pattern).as<uint32_t>();
+    P.pat_off = wheel_offset(a.base_n, a.pattern_present);
+    const int kind = pattern_kind(a.pattern_present);
+    if (ctx().wheel_present[kind] != a.pattern_present) throw Error{SQF2K_ECUDA, "wheel table not built"};
+    P.pattern = (kind == 2 ? c.pattern13 : kind == 1 ? c.pattern_b : c.pattern).as<uint32_t>();
     P.med = med_cache(a).buf.as<uint32_t>();
     P.tasks = reinterpret_cast<const uint2 *>(med_cache(a).buf.as<uint32_t>() + kMaxMed);
     P.tile_start = tile_start;

@@ -86,28 +86,32 @@ constexpr double kItemHitsRotate = 6.24;  // the same for the kind-2 schedule (t
 // p = 3, 5, 7 (and 11) are applied as one periodic word pattern: period
 // 9*25*49 words, or 9*25*49*121 with 11 (1.33 M words, 5.3 MB per copy,
 // L2-resident).  Taking 11 (541 hits per 2^16-slot tile, 27 % of the medium
-// scatter) out of the scatter measured 484.6 -> 467.7 ms per C5 call; building the larger table costs ~4 us per batch,
-// so domains below kPattern11MinSlots keep 11 in the scatter (C2: 0.088 vs
-// 0.092 ms per call).  SQF2K_PATTERN_11=0 never uses it.
+// scatter) out of the scatter measured 484.6 -> 467.7 ms per C5 call.  The
+// tables are wheel constants (tile.cu: ensure_wheel, built once per context
+// for the odd n = 1 and read at a per-batch word offset), so every domain
+// takes them: C2 0.088 -> 0.084 ms per call once the per-call build (9.5 us
+// for the 11 table) left the critical path.  SQF2K_PATTERN_11=0 never uses 11.
 constexpr bool kPattern11 = SQF2K_PATTERN_11 != 0;
 constexpr uint32_t kPatWords3 = 9 * 25 * 49;
 constexpr uint32_t kPatWordsMax = kPatWords3 * (kPattern11 ? 121 : 1);
 #ifndef SQF2K_PATTERN_11_MIN_SLOTS
-#define SQF2K_PATTERN_11_MIN_SLOTS (1ull << 30)
+#define SQF2K_PATTERN_11_MIN_SLOTS 0
 #endif
 constexpr uint64_t kPattern11MinSlots = SQF2K_PATTERN_11_MIN_SLOTS;
-// ... and 13 as well for the largest calls (SQF2K_PATTERN_13): period
-// 9*25*49*121*169 = 225.45 M words, one table per call (3.6 GB, stored as four
-// periods so that every tile start is 16-byte aligned without shifted copies,
-// read from HBM by the tile starts: 8 KB per 2^16-slot tile) and a per-batch
-// word offset; it takes the 388 hits per tile of p = 13 out of the scatter.
+// ... and 13 as well for fused calls from 2^28 slots (SQF2K_PATTERN_13):
+// period 9*25*49*121*169 = 225.45 M words (3.6 GB, stored as four periods so
+// that every tile start is 16-byte aligned without shifted copies, read from
+// HBM by the tile starts: 8 KB per 2^16-slot tile); it takes the 388 hits per
+// tile of p = 13 out of the scatter (A/B against the per-call tables of
+// before: C2 0.084 -> 0.083, C3 1.734 -> 1.705, C4 26.48 -> 25.59, C5
+// 407.7 -> 406.7 ms per call; smaller calls do not allocate it).
 #ifndef SQF2K_PATTERN_13
 #define SQF2K_PATTERN_13 1
 #endif
 constexpr bool kPattern13 = SQF2K_PATTERN_13 != 0 && kPattern11;
 constexpr uint32_t kPatPeriod13 = kPatWords3 * 121 * 169;
 #ifndef SQF2K_PATTERN_13_MIN_SLOTS
-#define SQF2K_PATTERN_13_MIN_SLOTS (1ull << 39)  // (C4, 2^39 slots: 26.70 -> 26.54 ms with kind 2)
+#define SQF2K_PATTERN_13_MIN_SLOTS (1ull << 28)
 #endif
 constexpr uint64_t kPattern13MinSlots = SQF2K_PATTERN_13_MIN_SLOTS;
 // index period of the table whose present mask is `present` (bit 3: prime
@@ -170,7 +174,7 @@ struct TileParams {
     uint32_t k_eff;      // passes inside the tile
     uint32_t k_max;      // run limit: escalate when k_max > k_eff
     uint32_t pat_words;          // period of the pattern table (pattern_words)
-    uint32_t pat_off;            // word offset of this batch in a per-call table (kind 2)
+    uint32_t pat_off;            // word offset of this batch's domain in the wheel table (wheel_offset)
     const uint32_t *pattern;     // p = 3, 5, 7 (11) mask by u-word mod pat_words (+ kTileWords
                                  // repeated words, so a tile never wraps)
     const uint32_t *med;         // q = p^2 of the medium primes
@@ -236,7 +240,6 @@ struct BatchArgs {
     const PrimeInfo *info;        // device split
     uint64_t n_primes_bound;      // host upper bound of the table size
     uint32_t pattern_present;     // bit i: prime 3/5/7/11/13 in the table
-    uint32_t pat_off;             // kind 2: word offset of this batch from the call's first
     const std::vector<uint32_t> *med_primes;
     unsigned long long *hist, *min_n, *esc, *esc_count, *fail, *fail_count;
     uint64_t esc_cap, fail_cap;

@@ -118,8 +118,8 @@ SmallSet small_set_upto_impl(uint64_t limit, int kind) {
 }
 
 // The pattern table kind of a call (tile.cuh): 11 joins the table for domains
-// of kPattern11MinSlots slots or more, 13 too (one per-call table) for fused
-// main-depth calls of kPattern13MinSlots or more.
+// of kPattern11MinSlots slots or more, 13 too (the 3.6 GB wheel table) for
+// fused main-depth calls of kPattern13MinSlots or more.
 SmallSet small_set_upto(uint64_t limit, uint64_t n_slots, bool allow13) {
     int kind = kPattern11 && n_slots >= kPattern11MinSlots ? 1 : 0;
     // (SQF2K_DEBUG_PAT13_MIN lowers the threshold: tests reach kind 2 on
@@ -226,12 +226,6 @@ void enqueue_verify(const VerifyPlan &pl) {
         a.base_n = (int64_t)A - 2 * (int64_t)H;
         a.U = H + sb;
         a.z = a.base_n < 1 ? (uint64_t)((1 - a.base_n) / 2) : 0;
-        // per-call pattern table (kind 2): this batch's words start s0 / 32
-        // words in (s0 is a multiple of the batch, hence of 128 slots, so
-        // tile starts stay 16-byte aligned)
-        a.pat_off = pattern_kind(a.pattern_present) == 2
-                        ? (uint32_t)((s0 / 32) % pattern_words(a.pattern_present))
-                        : 0u;
         if (pl.pipeline == 1) {  // two-pass: export [A - 2H, A + 2 sb), then scan it
             a.fused = false;
             a.scan_lo = 0;
