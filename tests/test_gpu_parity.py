@@ -458,11 +458,12 @@ def test_smallest_exponent_matches_scan_exponents():
 
 
 def test_pattern13_table_batches():
-    # the per-call p = 3..13 pattern table (kind 2, tile.cuh) normally serves
-    # only calls of >= 2^40 slots; SQF2K_DEBUG_PAT13_MIN lets a small
-    # multi-batch window use it, so every batch reads the table at its own
-    # word offset.  Results must equal the kind-1 path's (pinned to the
-    # reference's reports by test_run_verify_matches_large_goldens).
+    # the p = 3..13 wheel table (kind 2, tile.cuh) serves fused calls from
+    # 2^28 slots, the p <= 11 one (kind 1) the rest; SQF2K_DEBUG_PAT13_MIN
+    # moves the threshold, so the same windows run once on each kind -- every
+    # batch reading the wheel table at its own word offset (wheel_offset,
+    # tile.cu) -- and must agree (both are pinned to the reference's reports
+    # by test_run_verify_matches_large_goldens).
     import os
     import subprocess
     import sys
@@ -472,19 +473,22 @@ def test_pattern13_table_batches():
         "s, e = (1 << 50) - (1 << 34) + 1, (1 << 50) + 1\n"
         "out = [verify_range(s, e, 30, batch_slots=b) for b in (0, 1 << 30, 1 << 28, (1 << 28) + 32)]\n"
         "out += [verify_range(1, (1 << 33) + 1, 30, batch_slots=1 << 27)]\n"
+        "out += [verify_range(s0, s0 + (1 << 22), 30) for s0 in (3, (1 << 40) + 7, (1 << 45) + 12345)]\n"
         "print(json.dumps([[o.histogram, o.k_sum, sorted(o.record_candidates.items())] for o in out]))\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SQF2K_DEBUG_PAT13_MIN="0")
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
-                       timeout=600)
-    assert r.returncode == 0, r.stderr[-2000:]
-    got = json.loads(r.stdout.strip().splitlines()[-1])
-    s, e = (1 << 50) - (1 << 34) + 1, (1 << 50) + 1
-    want = verify_range(s, e, 30)
-    for g in got[:4]:
-        assert g == [want.histogram, want.k_sum, [list(x) for x in sorted(want.record_candidates.items())]]
-    base = verify_range(1, (1 << 33) + 1, 30)
-    assert got[4] == [base.histogram, base.k_sum, [list(x) for x in sorted(base.record_candidates.items())]]
+    got = {}
+    for kind, lim in (("kind2", "0"), ("kind1", str(1 << 62))):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root,
+                           env=dict(os.environ, SQF2K_DEBUG_PAT13_MIN=lim), capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        got[kind] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert got["kind2"] == got["kind1"]
+    for g in got["kind2"][1:4]:
+        assert g == got["kind2"][0]
+    want = verify_range((1 << 50) - (1 << 34) + 1, (1 << 50) + 1, 30)
+    assert got["kind2"][0] == [want.histogram, want.k_sum,
+                               [list(x) for x in sorted(want.record_candidates.items())]]
 
 
 @pytest.mark.parametrize("item,bias", [("3", "0"), ("16", "0.25"), ("20", "0.5")])

@@ -22,7 +22,7 @@ python $B > $O/${TAG}_launch_plain.log 2>&1 && \
       --log-file $O/${TAG}_launches_c5.csv python $B > $O/${TAG}_launch_ncu.log 2>&1; echo launches=$?
 # full captures: the fused tile kernel near 2^50, the window scan
 W="(1<<50)-(1<<38)+1"  # 2^37 odd slots: exactly one C5 batch
-# (SQF2K_DEBUG_PAT13_MIN=0: the window takes C5's per-call p <= 13 pattern
+# (SQF2K_DEBUG_PAT13_MIN=0: the window takes C5's p <= 13 wheel
 # table, i.e. exactly the kernel every C5 batch runs)
 export SQF2K_DEBUG_PAT13_MIN=0
 python tools/exp_time.py - "$W" "1<<50" > $O/${TAG}_plain_tile.log 2>&1 && \
